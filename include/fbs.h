@@ -1,0 +1,187 @@
+/*
+ * fbs.h — C ABI of the B200 (sm_100a) fast bilateral stereo (FBS) hot path.
+ *
+ * The library (paper_1807_02044_b200/libfbs.so) runs the method of
+ * arXiv 1807.02044 ("Real-Time Subpixel Fast Bilateral Stereo", PAPER.md):
+ *
+ *   NCC matching cost      Eq.(1)-(3)   P:L66-84   (block statistics pre-computed)
+ *   twin cost volumes      P:L86, P:L185           (left (u,v,d) == right (u-d,v,d))
+ *   bilateral aggregation  Eq.(6)-(8)   P:L118-132 (ω_d, ω_r tables pre-computed)
+ *   winner-take-all        P:L140, P:L201          (highest aggregated NCC over [d_min, d_max])
+ *   left-right consistency Eq.(9)       P:L148-153 (left image is the reference)
+ *   parabola subpixel      Eq.(10)
+ *
+ * "P:Lnn" is a line of PAPER.md; DESIGN.md §3 lists every reading taken where
+ * the paper is silent (borders, sentinels, tie-breaks, tolerances).
+ *
+ * Conventions shared by every entry point
+ *   - Images are uint8 grayscale, H rows of W pixels, row-major, pitch W
+ *     (R#3).  Disparity d >= 0 matches left (u,v) with right (u-d,v)
+ *     (Eq.(1): i_r(x-d, y)).
+ *   - The output disparity map is float32, H x W, pitch W.  Rejected or
+ *     undefined pixels hold FBS_INVALID (-1.0f).  Valid values lie in
+ *     [d_min, d_max].
+ *   - Unless stated otherwise, pointers are DEVICE pointers on the device that
+ *     was current when the handle was created, and calls are asynchronous on
+ *     the given stream (0 = legacy default stream): they enqueue work and
+ *     return.  The caller owns all I/O buffers and keeps them alive until the
+ *     stream work completes.  The library owns all scratch, allocated once in
+ *     fbs_create; fbs_compute never allocates or synchronises, so it can be
+ *     captured in a CUDA graph.
+ *   - A handle is NOT safe for concurrent use from several streams or threads
+ *     (its scratch is shared): use one handle per stream.
+ *   - Errors: every int-returning call returns FBS_OK (0) or a negative code;
+ *     fbs_last_error() gives a thread-local message.  Launch failures return
+ *     FBS_E_CUDA; asynchronous device faults surface at the caller's next
+ *     synchronisation (CUDA convention).  No C++ exception crosses the ABI.
+ */
+#ifndef FBS_H_
+#define FBS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FBS_INVALID (-1.0f) /* rejected / undefined pixel in a disparity map           */
+#define FBS_SENTINEL (-2.0f) /* undefined entry of a (debug) cost or aggregated volume  */
+
+enum {
+  FBS_OK = 0,
+  FBS_E_ARG = -1,         /* NULL pointer, bad handle, bad row range or batch size      */
+  FBS_E_PARAM = -2,       /* radius<0, sigma_s/sigma_r not finite & > 0, d_min<0,       */
+                          /* d_max<=d_min                                               */
+  FBS_E_DIM = -3,         /* W<3 or H<3 (image must hold one 3x3 NCC block)             */
+  FBS_E_UNSUPPORTED = -4, /* radius or disparity count beyond the compiled variants     */
+  FBS_E_CUDA = -5,        /* CUDA runtime error (launch, copy, device)                  */
+  FBS_E_OOM = -6          /* device allocation failed in fbs_create                     */
+};
+
+/* Opaque handle: frame geometry, parameters, weight tables, device scratch. */
+typedef struct fbs_ctx fbs_ctx;
+
+/* Stream type without pulling in cuda_runtime.h (same ABI as cudaStream_t). */
+typedef struct CUstream_st* fbs_stream_t;
+
+/*
+ * fbs_create — validate parameters, build the ω_d / ω_r tables (Eq.(7)(8),
+ * P:L199 "pre-calculated"), allocate all scratch on the current device.
+ *   W, H          frame size in pixels (>= 3 each)
+ *   d_min, d_max  inclusive disparity search range, 0 <= d_min < d_max
+ *   radius        ρ of Eq.(6): aggregation window (2ρ+1)^2; supported 1..FBS_MAX_RADIUS
+ *                 (0 is also accepted: the aggregation is then the identity)
+ *   sigma_s       γ_d of Eq.(7), used verbatim as exp(-r^2/γ_d^2)   (> 0, finite)
+ *   sigma_r       γ_r of Eq.(8), used verbatim as exp(-Δ^2/γ_r^2)   (> 0, finite)
+ * The NCC block half-width ϱ is fixed at 1 and the LRC tolerance at
+ * 1 pixel (R#17).  Returns NULL on error (reason: fbs_last_error()).
+ * Synchronises the device once (scratch initialisation); not graph-capturable.
+ */
+fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, float sigma_s, float sigma_r);
+
+/* fbs_destroy — free the handle and its scratch.  The caller must have
+ * synchronised all work enqueued with it.  NULL is a no-op. */
+void fbs_destroy(fbs_ctx* h);
+
+/* fbs_last_error — message of the last failing call on this thread ("" if none). */
+const char* fbs_last_error(void);
+
+/* Maximum supported aggregation radius ρ of this build. */
+#define FBS_MAX_RADIUS 6
+
+/*
+ * fbs_compute — the whole hot path for one rectified pair:
+ *   left, right  device uint8 [H][W]
+ *   disp_out     device float [H][W]: subpixel disparity d^s of the left image
+ *                (Eq.(10)) for LRC-consistent pixels (Eq.(9)), FBS_INVALID elsewhere.
+ * Asynchronous on `stream`; graph-capturable.
+ */
+int fbs_compute(fbs_ctx* h, const uint8_t* left, const uint8_t* right, float* disp_out,
+                fbs_stream_t stream);
+
+/*
+ * fbs_compute_rows — rows [row_begin, row_end) of what fbs_compute would write,
+ * bit-identical to them.  left/right are the FULL frames (device); disp_band
+ * is device float [(row_end-row_begin)][W].  Reads input rows
+ * [row_begin-ρ-1, row_end+ρ+1) only.  Used by the row-band multi-GPU
+ * partitioner.  0 <= row_begin < row_end <= H, else FBS_E_ARG.
+ */
+int fbs_compute_rows(fbs_ctx* h, const uint8_t* left, const uint8_t* right, int row_begin,
+                     int row_end, float* disp_band, fbs_stream_t stream);
+
+/*
+ * fbs_compute_batch — n independent pairs, frame i at left + i*H*W,
+ * right + i*H*W, output at disp_out + i*H*W (all device).  Equivalent to n
+ * fbs_compute calls in order on `stream`.  n >= 1.
+ */
+int fbs_compute_batch(fbs_ctx* h, const uint8_t* left, const uint8_t* right, int n,
+                      float* disp_out, fbs_stream_t stream);
+
+/*
+ * fbs_compute_host — end-to-end call on HOST buffers: copies left/right
+ * (host uint8 [H][W], ideally pinned) to the device, runs fbs_compute, copies
+ * the map back to disp_out (host float [H][W]) and synchronises `stream`
+ * before returning.  Blocking.
+ */
+int fbs_compute_host(fbs_ctx* h, const uint8_t* left, const uint8_t* right, float* disp_out,
+                     fbs_stream_t stream);
+
+/*
+ * fbs_debug_volumes — test-only export of the intermediate volumes, each
+ * device float [H][W][D] indexed ((v*W+u)*D + d-d_min), FBS_SENTINEL where
+ * undefined:
+ *   cost_l  c(u,v,d) of Eq.(1) (left reference)
+ *   cost_r  the right-reference twin, cost_r(u-d,v,d) == cost_l(u,v,d)
+ *   agg_l   Eq.(6) on cost_l guided by the left image
+ *   agg_r   Eq.(6) on cost_r guided by the right image
+ * Any output may be NULL.  Values are exactly those the production kernels
+ * compute.  Asynchronous.
+ */
+int fbs_debug_volumes(fbs_ctx* h, const uint8_t* left, const uint8_t* right, float* cost_l,
+                      float* cost_r, float* agg_l, float* agg_r, fbs_stream_t stream);
+
+/*
+ * fbs_debug_select — test-only: WTA on two given aggregated volumes (device
+ * float [H][W][D], FBS_SENTINEL = undefined), then LRC and subpixel.
+ *   disp_l, disp_r  device int32 [H][W] integer maps (-1 = INVALID), may be NULL
+ *   disp_out        device float [H][W] final map, may be NULL
+ * Asynchronous.
+ */
+int fbs_debug_select(fbs_ctx* h, const float* agg_l, const float* agg_r, int32_t* disp_l,
+                     int32_t* disp_r, float* disp_out, fbs_stream_t stream);
+
+/*
+ * fbs_debug_maps — test-only: fbs_compute that also exports the integer WTA
+ * maps of both sides (device int32 [H][W], -1 = INVALID; either may be NULL).
+ */
+int fbs_debug_maps(fbs_ctx* h, const uint8_t* left, const uint8_t* right, float* disp_out,
+                   int32_t* disp_l, int32_t* disp_r, fbs_stream_t stream);
+
+/*
+ * fbs_stats — counters of the last fbs_compute* call on this handle, for the
+ * bench's launch accounting (host ints, may be NULL):
+ *   launches   kernels launched per frame
+ * Returns FBS_OK.
+ */
+int fbs_stats(const fbs_ctx* h, int* launches);
+
+/*
+ * Live per-stage timing with CUDA events recorded on the launching stream.
+ * fbs_profile_enable(h, n): the next n fbs_compute* frames record an event at
+ * each stage boundary (n = 0 disables; n <= 65536; allocates the events, so
+ * call it outside graph capture).  fbs_profile_read(h, stage_ms, ncalls)
+ * waits for the recorded events, writes the summed milliseconds per stage to
+ * stage_ms[FBS_NSTAGES] (host) and the number of frames to *ncalls, then
+ * resets the counters.  Stages: 0 block statistics (2 launches), 1 twin cost
+ * volumes (2), 2 right aggregation+WTA (1), 3 left aggregation+WTA+LRC+
+ * subpixel (1).
+ */
+#define FBS_NSTAGES 4
+int fbs_profile_enable(fbs_ctx* h, int n);
+int fbs_profile_read(fbs_ctx* h, double* stage_ms, int* ncalls);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FBS_H_ */

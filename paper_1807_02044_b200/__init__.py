@@ -1,0 +1,260 @@
+"""Thin Python binding of libfbs.so — the B200 fast bilateral stereo (FBS) hot path.
+
+Argument marshalling only: every step of the method runs in the CUDA kernels
+behind the C ABI declared in ``include/fbs.h``.  PyTorch supplies device
+memory and streams.  There is no CPU fallback: if the extension is missing or
+no CUDA device is present, calls raise.
+
+Functions keep the C names (``fbs_create``, ``fbs_compute``, ...); the
+``FBS`` class is a convenience owner of one handle.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfbs.so")
+ROOT = os.path.dirname(_HERE)
+
+FBS_OK = 0
+FBS_E_ARG, FBS_E_PARAM, FBS_E_DIM, FBS_E_UNSUPPORTED, FBS_E_CUDA, FBS_E_OOM = -1, -2, -3, -4, -5, -6
+FBS_INVALID = -1.0
+FBS_SENTINEL = -2.0
+FBS_MAX_RADIUS = 6
+
+# every symbol include/fbs.h declares
+EXPORTS = ("fbs_create", "fbs_destroy", "fbs_last_error", "fbs_compute", "fbs_compute_rows",
+           "fbs_compute_batch", "fbs_compute_host", "fbs_debug_volumes", "fbs_debug_select",
+           "fbs_debug_maps", "fbs_stats", "fbs_profile_enable", "fbs_profile_read")
+FBS_NSTAGES = 4
+STAGES = ("stats", "cost", "agg_r", "agg_l")
+
+_lib = None
+
+
+class FbsError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"FBS error {code}: {msg}")
+        self.code = code
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libfbs.so (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    P, I, F = ctypes.c_void_p, ctypes.c_int, ctypes.c_float
+    lib.fbs_create.argtypes = [I, I, I, I, I, F, F]
+    lib.fbs_create.restype = P
+    lib.fbs_destroy.argtypes = [P]
+    lib.fbs_destroy.restype = None
+    lib.fbs_last_error.argtypes = []
+    lib.fbs_last_error.restype = ctypes.c_char_p
+    lib.fbs_compute.argtypes = [P, P, P, P, P]
+    lib.fbs_compute_rows.argtypes = [P, P, P, I, I, P, P]
+    lib.fbs_compute_batch.argtypes = [P, P, P, I, P, P]
+    lib.fbs_compute_host.argtypes = [P, P, P, P, P]
+    lib.fbs_debug_volumes.argtypes = [P, P, P, P, P, P, P, P]
+    lib.fbs_debug_select.argtypes = [P, P, P, P, P, P, P]
+    lib.fbs_debug_maps.argtypes = [P, P, P, P, P, P, P]
+    lib.fbs_stats.argtypes = [P, ctypes.POINTER(I)]
+    lib.fbs_profile_enable.argtypes = [P, I]
+    lib.fbs_profile_read.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I)]
+    for name in ("fbs_compute", "fbs_compute_rows", "fbs_compute_batch", "fbs_compute_host",
+                 "fbs_debug_volumes", "fbs_debug_select", "fbs_debug_maps", "fbs_stats",
+                 "fbs_profile_enable", "fbs_profile_read"):
+        getattr(lib, name).restype = I
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    return load_library().fbs_last_error().decode()
+
+
+def _check(rc: int):
+    if rc != FBS_OK:
+        raise FbsError(rc, last_error())
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+# ---------------------------------------------------------------------------
+# C-named wrappers
+
+def fbs_create(W: int, H: int, d_min: int, d_max: int, radius: int, sigma_s: float, sigma_r: float):
+    h = load_library().fbs_create(W, H, d_min, d_max, radius, sigma_s, sigma_r)
+    if not h:
+        raise FbsError(FBS_E_PARAM, last_error())
+    return ctypes.c_void_p(h)
+
+
+def fbs_destroy(h) -> None:
+    load_library().fbs_destroy(h)
+
+
+def fbs_compute(h, left, right, disp_out, stream=None) -> None:
+    _check(load_library().fbs_compute(h, _ptr(left), _ptr(right), _ptr(disp_out), _stream(stream)))
+
+
+def fbs_compute_rows(h, left, right, row_begin: int, row_end: int, disp_band, stream=None) -> None:
+    _check(load_library().fbs_compute_rows(h, _ptr(left), _ptr(right), row_begin, row_end,
+                                           _ptr(disp_band), _stream(stream)))
+
+
+def fbs_compute_batch(h, left, right, n: int, disp_out, stream=None) -> None:
+    _check(load_library().fbs_compute_batch(h, _ptr(left), _ptr(right), n, _ptr(disp_out),
+                                            _stream(stream)))
+
+
+def fbs_compute_host(h, left, right, disp_out, stream=None) -> None:
+    """Host (CPU, ideally pinned) uint8 inputs and float output; blocking."""
+    _check(load_library().fbs_compute_host(h, _ptr(left), _ptr(right), _ptr(disp_out),
+                                           _stream(stream)))
+
+
+def fbs_debug_volumes(h, left, right, cost_l=None, cost_r=None, agg_l=None, agg_r=None,
+                      stream=None) -> None:
+    _check(load_library().fbs_debug_volumes(h, _ptr(left), _ptr(right), _ptr(cost_l), _ptr(cost_r),
+                                            _ptr(agg_l), _ptr(agg_r), _stream(stream)))
+
+
+def fbs_debug_select(h, agg_l, agg_r, disp_l=None, disp_r=None, disp_out=None, stream=None) -> None:
+    _check(load_library().fbs_debug_select(h, _ptr(agg_l), _ptr(agg_r), _ptr(disp_l), _ptr(disp_r),
+                                           _ptr(disp_out), _stream(stream)))
+
+
+def fbs_debug_maps(h, left, right, disp_out, disp_l=None, disp_r=None, stream=None) -> None:
+    _check(load_library().fbs_debug_maps(h, _ptr(left), _ptr(right), _ptr(disp_out), _ptr(disp_l),
+                                         _ptr(disp_r), _stream(stream)))
+
+
+def fbs_stats(h) -> dict:
+    n = ctypes.c_int(0)
+    _check(load_library().fbs_stats(h, ctypes.byref(n)))
+    return {"launches": n.value}
+
+
+def fbs_profile_enable(h, n: int) -> None:
+    _check(load_library().fbs_profile_enable(h, n))
+
+
+def fbs_profile_read(h) -> tuple[dict, int]:
+    """Summed milliseconds per stage over the profiled frames, and their count."""
+    arr = (ctypes.c_double * FBS_NSTAGES)()
+    n = ctypes.c_int(0)
+    _check(load_library().fbs_profile_read(h, arr, ctypes.byref(n)))
+    return dict(zip(STAGES, list(arr))), n.value
+
+
+# ---------------------------------------------------------------------------
+class FBS:
+    """Owner of one handle (one per stream).  Inputs/outputs are torch tensors
+    on the handle's device: uint8 [H, W] pairs in, float32 [H, W] map out."""
+
+    def __init__(self, W: int, H: int, d_min: int, d_max: int, radius: int, sigma_s: float,
+                 sigma_r: float, device=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1807_02044_b200 needs a CUDA device (sm_100a); no CPU fallback")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.W, self.H, self.d_min, self.d_max, self.radius = W, H, d_min, d_max, radius
+        self.sigma_s, self.sigma_r = sigma_s, sigma_r
+        self.D = d_max - d_min + 1
+        with torch.cuda.device(self.device):
+            self.h = fbs_create(W, H, d_min, d_max, radius, sigma_s, sigma_r)
+
+    def close(self):
+        if getattr(self, "h", None):
+            fbs_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _chk(self, *ts):
+        for t in ts:
+            if t is not None:
+                assert t.is_cuda and t.is_contiguous(), "device, contiguous tensors required"
+
+    def compute(self, left, right, out=None, stream=None):
+        import torch
+        self._chk(left, right)
+        if out is None:
+            out = torch.empty((self.H, self.W), dtype=torch.float32, device=left.device)
+        fbs_compute(self.h, left, right, out, stream)
+        return out
+
+    def compute_rows(self, left, right, r0: int, r1: int, out=None, stream=None):
+        import torch
+        self._chk(left, right)
+        if out is None:
+            out = torch.empty((r1 - r0, self.W), dtype=torch.float32, device=left.device)
+        fbs_compute_rows(self.h, left, right, r0, r1, out, stream)
+        return out
+
+    def compute_batch(self, left, right, out=None, stream=None):
+        import torch
+        self._chk(left, right)
+        n = left.shape[0]
+        if out is None:
+            out = torch.empty((n, self.H, self.W), dtype=torch.float32, device=left.device)
+        fbs_compute_batch(self.h, left, right, n, out, stream)
+        return out
+
+    def compute_host(self, left, right, out=None, stream=None):
+        import torch
+        if out is None:
+            out = torch.empty((self.H, self.W), dtype=torch.float32, pin_memory=True)
+        fbs_compute_host(self.h, left, right, out, stream)
+        return out
+
+    def volumes(self, left, right, stream=None):
+        import torch
+        shp = (self.H, self.W, self.D)
+        vols = [torch.empty(shp, dtype=torch.float32, device=left.device) for _ in range(4)]
+        fbs_debug_volumes(self.h, left, right, *vols, stream=stream)
+        return vols
+
+    def maps(self, left, right, stream=None):
+        import torch
+        out = torch.empty((self.H, self.W), dtype=torch.float32, device=left.device)
+        dl = torch.empty((self.H, self.W), dtype=torch.int32, device=left.device)
+        dr = torch.empty_like(dl)
+        fbs_debug_maps(self.h, left, right, out, dl, dr, stream)
+        return out, dl, dr
+
+    def select(self, agg_l, agg_r, stream=None):
+        import torch
+        out = torch.empty((self.H, self.W), dtype=torch.float32, device=agg_l.device)
+        dl = torch.empty((self.H, self.W), dtype=torch.int32, device=agg_l.device)
+        dr = torch.empty_like(dl)
+        fbs_debug_select(self.h, agg_l, agg_r, dl, dr, out, stream)
+        return out, dl, dr
+
+    def profile_enable(self, n: int):
+        fbs_profile_enable(self.h, n)
+
+    def profile_read(self):
+        return fbs_profile_read(self.h)
+
+    def launches_per_frame(self) -> int:
+        return fbs_stats(self.h)["launches"]

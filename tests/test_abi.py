@@ -1,0 +1,86 @@
+"""CPU-side checks of the C ABI: libfbs.so builds for sm_100a, loads, exports
+every function include/fbs.h declares, and rejects bad parameters before
+touching the device (no compute call here)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1807_02044_b200 import build
+    path = build.build()
+    import paper_1807_02044_b200 as fbs
+    return fbs.load_library(path)
+
+
+def header_functions():
+    txt = open(os.path.join(ROOT, "include", "fbs.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(fbs_[a-z_]+)\s*\(", txt)))
+
+
+def test_exports_every_declared_symbol(lib):
+    import paper_1807_02044_b200 as fbs
+    names = header_functions()
+    assert len(names) >= 10
+    assert sorted(names) == sorted(fbs.EXPORTS)
+    for n in names:
+        assert hasattr(lib, n), n
+    out = subprocess.run(["nm", "-D", "--defined-only", fbs.LIB_PATH], capture_output=True, text=True).stdout
+    for n in names:
+        assert re.search(rf"\bT {n}\b", out), n
+
+
+def test_built_for_sm100a():
+    import paper_1807_02044_b200 as fbs
+    out = subprocess.run(["cuobjdump", "--list-elf", fbs.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_sass_uses_ffma2():
+    """The aggregation inner loop issues FFMA2 with a broadcast scalar weight."""
+    import paper_1807_02044_b200 as fbs
+    out = subprocess.run(["cuobjdump", "-sass", "-fun", "_ZN3fbs5k_aggILi0ELi4EEEvNS_7AggArgsE",
+                          fbs.LIB_PATH], capture_output=True, text=True).stdout
+    assert out.count("FFMA2") >= 100
+    assert re.search(r"FFMA2 R\d+, R\d+\.F32, R\d+\.F32x2", out)
+
+
+@pytest.mark.parametrize("args,code", [
+    ((2, 10, 0, 5, 1, 1.0, 1.0), -3),
+    ((10, 2, 0, 5, 1, 1.0, 1.0), -3),
+    ((10, 10, -1, 5, 1, 1.0, 1.0), -2),
+    ((10, 10, 5, 5, 1, 1.0, 1.0), -2),
+    ((10, 10, 0, 5, -1, 1.0, 1.0), -2),
+    ((10, 10, 0, 5, 1, 0.0, 1.0), -2),
+    ((10, 10, 0, 5, 1, 1.0, float("nan")), -2),
+    ((10, 10, 0, 5, 7, 1.0, 1.0), -4),
+])
+def test_create_rejects_bad_params(lib, args, code):
+    h = lib.fbs_create(*args)
+    assert not h
+    assert lib.fbs_last_error().decode().startswith("fbs_create")
+
+
+def test_null_handle_calls_fail_cleanly(lib):
+    assert lib.fbs_compute(None, None, None, None, None) == -1
+    assert lib.fbs_compute_rows(None, None, None, 0, 1, None, None) == -1
+    assert lib.fbs_stats(None, None) == -1
+    lib.fbs_destroy(None)
+
+
+def test_binding_fails_loudly_without_library(tmp_path):
+    import paper_1807_02044_b200 as fbs
+    saved = fbs._lib
+    fbs._lib = None
+    try:
+        with pytest.raises(ImportError):
+            fbs.load_library(str(tmp_path / "missing.so"))
+    finally:
+        fbs._lib = saved
