@@ -202,6 +202,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     step_ms = [a.elapsed_time(b) for a, b in ev]
     tot_ms = sum(step_ms)
     stage_ms, nprof = m.profile_read()
+    n_fast, n_slow = m.tile_stats()
     m.profile_enable(0)
     t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -237,25 +238,26 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     if rank != 0:
         return None
-    # ---- roofline of the dominant kernel (aggregation + WTA, one launch per side) ----
+    # ---- roofline of the dominant kernel (aggregation + WTA, both sides in one launch) ----
     peak, peak_src = load_peak_fp32()
-    agg_ms = (stage_ms["agg_r"] + stage_ms["agg_l"]) / (2 * max(1, nprof))
+    agg_ms = stage_ms["agg"] / max(1, nprof)
     if banded:
         rows = fdist.band_range(cfg.H, rank, world)
         frac_rows = (rows[1] - rows[0]) / cfg.H
     else:
         frac_rows = 1.0
-    achieved = useful_flops_per_side(cfg) * frac_rows / (agg_ms * 1e-3) / 1e12
+    achieved = 2 * useful_flops_per_side(cfg) * frac_rows / (agg_ms * 1e-3) / 1e12
     tot_stage = sum(stage_ms.values())
     roof = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "traffic": load_traffic(cfg.name),
-            "kernel": "k_agg (bilateral aggregation + WTA, per side)",
+            "kernel": "k_agg (bilateral aggregation + WTA, both sides per launch)",
             "avg_launch_ms": round(agg_ms, 5),
-            "share_of_step": round((stage_ms["agg_r"] + stage_ms["agg_l"]) / tot_stage, 3) if tot_stage else None,
+            "share_of_step": round(stage_ms["agg"] / tot_stage, 3) if tot_stage else None,
             "stage_ms_per_frame": {k: round(v / max(1, nprof), 5) for k, v in stage_ms.items()},
             "peak_source": f"148 SM x 128 FP32 lanes x 2 x {peak_src} (nominal); "
                            "FFMA2 microbenchmark 66.9 TFLOP/s (DESIGN.md §6)",
-            "useful_work": "numerator FMAs of Eq.(6): W*H*D*(2rho+1)^2 per side"}
+            "useful_work": "numerator FMAs of Eq.(6): 2 sides x W*H*D*(2rho+1)^2 per launch",
+            "slow_path_fraction": round(n_slow / max(1, n_fast + n_slow), 4)}
     base = None
     if world == 1 and not args.no_extras:
         base = cpu_baseline(cfg, frames_np[:1] * 3 if not banded else frames_np[:1])

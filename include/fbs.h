@@ -173,13 +173,22 @@ int fbs_stats(const fbs_ctx* h, int* launches);
  * call it outside graph capture).  fbs_profile_read(h, stage_ms, ncalls)
  * waits for the recorded events, writes the summed milliseconds per stage to
  * stage_ms[FBS_NSTAGES] (host) and the number of frames to *ncalls, then
- * resets the counters.  Stages: 0 block statistics (2 launches), 1 twin cost
- * volumes (2), 2 right aggregation+WTA (1), 3 left aggregation+WTA+LRC+
- * subpixel (1).
+ * resets the counters.  Stages (one launch each): 0 block statistics + twin
+ * cost volumes of both sides, 1 bilateral aggregation + WTA of both sides,
+ * 2 LRC + subpixel.
  */
-#define FBS_NSTAGES 4
+#define FBS_NSTAGES 3
 int fbs_profile_enable(fbs_ctx* h, int n);
 int fbs_profile_read(fbs_ctx* h, double* stage_ms, int* ncalls);
+
+/*
+ * fbs_tile_stats — how many (CTA tile, disparity block) units of the
+ * aggregation took the fast path (denominator = Σ w', d-independent) and the
+ * exact slow path (explicit denominator: frame edges, textureless regions)
+ * during the frames profiled since the last call (counting is on while
+ * fbs_profile_enable is active).  Synchronises the device; resets the counts.
+ */
+int fbs_tile_stats(fbs_ctx* h, long long* fast, long long* slow);
 
 #ifdef __cplusplus
 }

@@ -14,7 +14,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfbs.so")
+LIB_PATH = os.environ.get("FBS_LIB", os.path.join(_HERE, "libfbs.so"))  # FBS_LIB: A/B experiments
 ROOT = os.path.dirname(_HERE)
 
 FBS_OK = 0
@@ -26,9 +26,9 @@ FBS_MAX_RADIUS = 6
 # every symbol include/fbs.h declares
 EXPORTS = ("fbs_create", "fbs_destroy", "fbs_last_error", "fbs_compute", "fbs_compute_rows",
            "fbs_compute_batch", "fbs_compute_host", "fbs_debug_volumes", "fbs_debug_select",
-           "fbs_debug_maps", "fbs_stats", "fbs_profile_enable", "fbs_profile_read")
-FBS_NSTAGES = 4
-STAGES = ("stats", "cost", "agg_r", "agg_l")
+           "fbs_debug_maps", "fbs_stats", "fbs_profile_enable", "fbs_profile_read", "fbs_tile_stats")
+FBS_NSTAGES = 3
+STAGES = ("cost", "agg", "finalize")
 
 _lib = None
 
@@ -64,9 +64,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.fbs_stats.argtypes = [P, ctypes.POINTER(I)]
     lib.fbs_profile_enable.argtypes = [P, I]
     lib.fbs_profile_read.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I)]
+    lib.fbs_tile_stats.argtypes = [P, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong)]
     for name in ("fbs_compute", "fbs_compute_rows", "fbs_compute_batch", "fbs_compute_host",
                  "fbs_debug_volumes", "fbs_debug_select", "fbs_debug_maps", "fbs_stats",
-                 "fbs_profile_enable", "fbs_profile_read"):
+                 "fbs_profile_enable", "fbs_profile_read", "fbs_tile_stats"):
         getattr(lib, name).restype = I
     _lib = lib
     return lib
@@ -162,6 +163,12 @@ def fbs_profile_read(h) -> tuple[dict, int]:
     return dict(zip(STAGES, list(arr))), n.value
 
 
+def fbs_tile_stats(h) -> tuple[int, int]:
+    f, s = ctypes.c_longlong(0), ctypes.c_longlong(0)
+    _check(load_library().fbs_tile_stats(h, ctypes.byref(f), ctypes.byref(s)))
+    return f.value, s.value
+
+
 # ---------------------------------------------------------------------------
 class FBS:
     """Owner of one handle (one per stream).  Inputs/outputs are torch tensors
@@ -255,6 +262,9 @@ class FBS:
 
     def profile_read(self):
         return fbs_profile_read(self.h)
+
+    def tile_stats(self):
+        return fbs_tile_stats(self.h)
 
     def launches_per_frame(self) -> int:
         return fbs_stats(self.h)["launches"]

@@ -2,11 +2,10 @@
 //
 // Host side: parameter validation, ω_d / ω_r tables (Eq.(7)(8), built in
 // double and rounded once to fp32, "pre-calculated"), scratch
-// allocation, and the launch sequence per frame:
-//   k_stats(L), k_stats(R)         block statistics     Eq.(2)(3)
-//   k_cost<L>, k_cost<R>           twin cost volumes    Eq.(1)
-//   k_agg<R>                       right aggregation + WTA -> d_R
-//   k_agg<L>                       left aggregation + WTA + LRC + subpixel -> disp_out
+// allocation, and the launch sequence per frame (3 launches):
+//   k_cost      block statistics + twin cost volumes, both sides   Eq.(1)-(3)
+//   k_agg       aggregation + WTA, both sides                      Eq.(6)-(8)
+//   k_finalize  LRC + subpixel -> disp_out                         Eq.(9)(10)
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -19,29 +18,30 @@
 using namespace fbs;
 
 struct fbs_ctx {
-  int W, H, d_min, d_max, D, Dp, R, Wv, Hv;
+  int W, H, d_min, d_max, D, nblk, R, Wv, Hv;
   float sigma_s, sigma_r;
   int device;
   float wd[(2 * kMaxRadius + 1) * (2 * kMaxRadius + 1)];
   float wr[256];
   // scratch
-  uint32_t *PL, *PR;
-  int32_t *SL, *SR;
-  float *rL, *rR;
   uint8_t *defL, *defR;
+  uint32_t *bitsL, *bitsR;
+  int Wb;
   float *volL, *volR;
-  int32_t* dR;
+  int32_t *dL, *dR;
+  float4* c3;        // left WTA (c(d*), c(d*-1), c(d*+1))
   uint8_t *hL, *hR;  // device staging for fbs_compute_host
   float* hOut;
-  float* c3;         // debug select scratch [H][W][3]
-  int32_t* dLtmp;
+  unsigned long long* tile_stats;  // device [2], counting when prof_ev is set
   int launches;
-  // live profiling (fbs_profile_enable): 5 events per frame
+  // live profiling (fbs_profile_enable): kEv events per frame
   cudaEvent_t* prof_ev;
   int prof_cap, prof_n;
 };
 
 static thread_local std::string g_err;
+
+static constexpr int kEv = FBS_NSTAGES + 1;
 
 static int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -56,8 +56,8 @@ static int cuda_check(cudaError_t e, const char* what) {
 extern "C" const char* fbs_last_error(void) { return g_err.c_str(); }
 
 static void free_all(fbs_ctx* h) {
-  void* ptrs[] = {h->PL, h->PR, h->SL, h->SR, h->rL, h->rR, h->defL, h->defR, h->volL,
-                  h->volR, h->dR, h->hL, h->hR, h->hOut, h->c3, h->dLtmp};
+  void* ptrs[] = {h->defL, h->defR, h->bitsL, h->bitsR, h->volL, h->volR, h->dL, h->dR, h->c3, h->hL, h->hR, h->hOut,
+                  h->tile_stats};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -89,7 +89,7 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
   }
   std::memset(h, 0, sizeof(*h));
   h->W = W; h->H = H; h->d_min = d_min; h->d_max = d_max; h->D = d_max - d_min + 1;
-  h->Dp = (h->D + kDB - 1) / kDB * kDB;
+  h->nblk = (h->D + kDB - 1) / kDB;
   h->R = radius;
   h->Wv = (W + kTX - 1) / kTX * kTX + 2 * radius;
   h->Hv = (H + kTY - 1) / kTY * kTY + kTY + 2 * radius;
@@ -104,19 +104,19 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
   for (int a = 0; a < 256; ++a) h->wr[a] = (float)std::exp(-(double)a * a / (gr * gr));
 
   const size_t npix = (size_t)W * H;
-  const size_t nvol = (size_t)h->Hv * h->Wv * h->Dp;
+  const size_t nvol = (size_t)h->Hv * h->Wv * h->nblk * kDB;
   bool ok = true;
-  ok &= cudaMalloc(&h->PL, npix * 4) == cudaSuccess;
-  ok &= cudaMalloc(&h->PR, npix * 4) == cudaSuccess;
-  ok &= cudaMalloc(&h->SL, npix * 4) == cudaSuccess;
-  ok &= cudaMalloc(&h->SR, npix * 4) == cudaSuccess;
-  ok &= cudaMalloc(&h->rL, npix * 4) == cudaSuccess;
-  ok &= cudaMalloc(&h->rR, npix * 4) == cudaSuccess;
+  h->Wb = (W + kCX - 1) / kCX * (kCX / 32);
   ok &= cudaMalloc(&h->defL, npix) == cudaSuccess;
+  ok &= cudaMalloc(&h->bitsL, (size_t)H * h->Wb * 4) == cudaSuccess;
+  ok &= cudaMalloc(&h->bitsR, (size_t)H * h->Wb * 4) == cudaSuccess;
   ok &= cudaMalloc(&h->defR, npix) == cudaSuccess;
   ok &= cudaMalloc(&h->volL, nvol * 4) == cudaSuccess;
   ok &= cudaMalloc(&h->volR, nvol * 4) == cudaSuccess;
+  ok &= cudaMalloc(&h->dL, npix * 4) == cudaSuccess;
   ok &= cudaMalloc(&h->dR, npix * 4) == cudaSuccess;
+  ok &= cudaMalloc(&h->c3, npix * sizeof(float4)) == cudaSuccess;
+  ok &= cudaMalloc(&h->tile_stats, 2 * sizeof(unsigned long long)) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
     free_all(h);
@@ -127,16 +127,21 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
   // margins (and never-written rows) of the volumes hold SENT
   k_fill<<<1184, 256>>>(h->volL, nvol, kSent);
   k_fill<<<1184, 256>>>(h->volR, nvol, kSent);
+  cudaMemset(h->tile_stats, 0, 2 * sizeof(unsigned long long));
+  cudaMemset(h->dL, 0xff, npix * 4);
   cudaMemset(h->dR, 0xff, npix * 4);
+  cudaMemset(h->defL, 0, npix);
+  cudaMemset(h->defR, 0, npix);
+  cudaMemset(h->bitsL, 0, (size_t)H * h->Wb * 4);
+  cudaMemset(h->bitsR, 0, (size_t)H * h->Wb * 4);
   if (cuda_check(cudaDeviceSynchronize(), "fbs_create init") != FBS_OK) {
     free_all(h);
     delete h;
     return nullptr;
   }
   // opt-in shared memory for every aggregation variant
-#define FBS_SMEM_ATTR(RR)                                                                      \
-  cudaFuncSetAttribute(k_agg<0, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(AggSmem<RR>)); \
-  cudaFuncSetAttribute(k_agg<1, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(AggSmem<RR>));
+#define FBS_SMEM_ATTR(RR) \
+  cudaFuncSetAttribute(k_agg<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(AggSmem<RR>));
   FBS_SMEM_ATTR(0) FBS_SMEM_ATTR(1) FBS_SMEM_ATTR(2) FBS_SMEM_ATTR(3) FBS_SMEM_ATTR(4)
   FBS_SMEM_ATTR(5) FBS_SMEM_ATTR(6)
 #undef FBS_SMEM_ATTR
@@ -150,7 +155,7 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
 
 static void prof_free(fbs_ctx* h) {
   if (h->prof_ev) {
-    for (int i = 0; i < 5 * h->prof_cap; ++i) cudaEventDestroy(h->prof_ev[i]);
+    for (int i = 0; i < kEv * h->prof_cap; ++i) cudaEventDestroy(h->prof_ev[i]);
     delete[] h->prof_ev;
   }
   h->prof_ev = nullptr;
@@ -167,77 +172,66 @@ extern "C" void fbs_destroy(fbs_ctx* h) {
 // ---------------------------------------------------------------------------
 static void fill_agg_args(const fbs_ctx* h, AggArgs& a) {
   a.W = h->W; a.H = h->H; a.D = h->D; a.d_min = h->d_min; a.d_max = h->d_max;
-  a.Dp = h->Dp; a.Wv = h->Wv;
+  a.nblk = h->nblk; a.Wv = h->Wv;
   std::memcpy(a.wd, h->wd, sizeof(a.wd));
   std::memcpy(a.wr, h->wr, sizeof(a.wr));
 }
 
-template <int SIDE>
 static void launch_agg(const fbs_ctx* h, const AggArgs& a, cudaStream_t s) {
-  dim3 grid((h->W + kTX - 1) / kTX, (a.r1 - a.r0 + kTY - 1) / kTY);
+  dim3 grid((h->W + kTX - 1) / kTX, (a.r1 - a.r0 + kTY - 1) / kTY, 2);
   switch (h->R) {
 #define FBS_CASE(RR) \
-  case RR: k_agg<SIDE, RR><<<grid, kThreads, sizeof(AggSmem<RR>), s>>>(a); break;
+  case RR: k_agg<RR><<<grid, kThreads, sizeof(AggSmem<RR>), s>>>(a); break;
     FBS_CASE(0) FBS_CASE(1) FBS_CASE(2) FBS_CASE(3) FBS_CASE(4) FBS_CASE(5) FBS_CASE(6)
 #undef FBS_CASE
   }
 }
 
-// Rows [r0, r1) of the output; all stages restricted to the rows they need.
+// Rows [r0, r1) of the output; every stage restricted to the rows it needs.
 static int run_rows(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0, int r1, float* out,
-                    int32_t* dL_dbg, int32_t* dR_dbg, float* aggL_exp, float* aggR_exp,
-                    cudaStream_t s) {
+                    float* aggL_exp, float* aggR_exp, cudaStream_t s) {
   const int W = h->W, H = h->H, R = h->R;
-  const int c0 = std::max(0, r0 - R), c1 = std::min(H, r1 + R);      // cost rows
-  const int s0 = std::max(0, c0 - 1), s1 = std::min(H, c1 + 1);      // stats rows
+  const int c0 = std::max(0, r0 - R), c1 = std::min(H, r1 + R);  // cost rows
   h->launches = 0;
   cudaEvent_t* ev = nullptr;
-  if (h->prof_ev && h->prof_n < h->prof_cap) ev = h->prof_ev + 5 * h->prof_n++;
+  if (h->prof_ev && h->prof_n < h->prof_cap) ev = h->prof_ev + kEv * h->prof_n++;
   if (ev) cudaEventRecord(ev[0], s);
   {
-    dim3 blk(128), grd((W + 127) / 128, s1 - s0);
-    k_stats<<<grd, blk, 0, s>>>(L, W, H, s0, s1, h->PL, h->SL, h->rL, h->defL);
-    k_stats<<<grd, blk, 0, s>>>(Rimg, W, H, s0, s1, h->PR, h->SR, h->rR, h->defR);
-    h->launches += 2;
+    CostArgs ca;
+    ca.W = W; ca.H = H; ca.D = h->D; ca.d_min = h->d_min; ca.nblk = h->nblk; ca.Wv = h->Wv; ca.R = R;
+    ca.r0 = c0; ca.r1 = c1;
+    ca.L = L; ca.Rimg = Rimg; ca.volL = h->volL; ca.volR = h->volR; ca.defL = h->defL; ca.defR = h->defR;
+    ca.bitsL = h->bitsL; ca.bitsR = h->bitsR; ca.Wb = h->Wb;
+    const int ocount = kCX + h->nblk * kDB - 1;
+    const size_t smem = (size_t)(kCX + ocount) * (sizeof(uint4) + sizeof(float));
+    dim3 grd((W + kCX - 1) / kCX, c1 - c0, 2);
+    k_cost<<<grd, 256, smem, s>>>(ca);
+    h->launches += 1;
   }
   if (ev) cudaEventRecord(ev[1], s);
-  {
-    CostArgs ca;
-    ca.W = W; ca.H = H; ca.D = h->D; ca.d_min = h->d_min; ca.Dp = h->Dp; ca.Wv = h->Wv; ca.R = R;
-    ca.r0 = c0; ca.r1 = c1;
-    ca.PL = h->PL; ca.PR = h->PR; ca.SL = h->SL; ca.SR = h->SR; ca.rL = h->rL; ca.rR = h->rR;
-    ca.defL = h->defL; ca.defR = h->defR;
-    dim3 grd((W + 7) / 8, c1 - c0, h->Dp / kDB);
-    ca.vol = h->volL;
-    k_cost<0><<<grd, 256, 0, s>>>(ca);
-    ca.vol = h->volR;
-    k_cost<1><<<grd, 256, 0, s>>>(ca);
-    h->launches += 2;
-  }
-  if (ev) cudaEventRecord(ev[2], s);
   AggArgs a;
   fill_agg_args(h, a);
   a.r0 = r0; a.r1 = r1;
-  // right pass first: the LRC of the left pass reads d_R (row-local, Eq.(9))
-  a.vol = h->volR; a.guide = Rimg; a.def_self = h->defR; a.def_other = h->defL;
-  a.disp_int = dR_dbg ? dR_dbg : h->dR; a.disp_r = nullptr; a.disp_out = nullptr;
-  a.agg_export = aggR_exp;
-  launch_agg<1>(h, a, s);
+  a.volL = h->volL; a.volR = h->volR; a.L = L; a.Rimg = Rimg; a.defL = h->defL; a.defR = h->defR;
+  a.bitsL = h->bitsL; a.bitsR = h->bitsR; a.Wb = h->Wb;
+  a.dL = h->dL; a.dR = h->dR; a.c3 = h->c3; a.exportL = aggL_exp; a.exportR = aggR_exp;
+  a.tile_stats = ev ? h->tile_stats : nullptr;
+  launch_agg(h, a, s);
+  h->launches += 1;
+  if (ev) cudaEventRecord(ev[2], s);
+  {
+    dim3 grd((W + 127) / 128, r1 - r0);
+    k_finalize<<<grd, 128, 0, s>>>(h->dL, h->dR, h->c3, W, r0, r1, h->d_min, h->d_max, out);
+    h->launches += 1;
+  }
   if (ev) cudaEventRecord(ev[3], s);
-  a.vol = h->volL; a.guide = L; a.def_self = h->defL; a.def_other = h->defR;
-  a.disp_int = dL_dbg; a.disp_r = dR_dbg ? dR_dbg : h->dR; a.disp_out = out;
-  a.agg_export = aggL_exp;
-  launch_agg<0>(h, a, s);
-  if (ev) cudaEventRecord(ev[4], s);
-  h->launches += 2;
   return cuda_check(cudaGetLastError(), "fbs launch");
 }
 
 extern "C" int fbs_compute(fbs_ctx* h, const uint8_t* left, const uint8_t* right, float* disp_out,
                            fbs_stream_t stream) {
   if (!h || !left || !right || !disp_out) return fail(FBS_E_ARG, "fbs_compute: NULL argument");
-  return run_rows(h, left, right, 0, h->H, disp_out, nullptr, nullptr, nullptr, nullptr,
-                  (cudaStream_t)stream);
+  return run_rows(h, left, right, 0, h->H, disp_out, nullptr, nullptr, (cudaStream_t)stream);
 }
 
 extern "C" int fbs_compute_rows(fbs_ctx* h, const uint8_t* left, const uint8_t* right, int row_begin,
@@ -245,8 +239,7 @@ extern "C" int fbs_compute_rows(fbs_ctx* h, const uint8_t* left, const uint8_t* 
   if (!h || !left || !right || !disp_band) return fail(FBS_E_ARG, "fbs_compute_rows: NULL argument");
   if (row_begin < 0 || row_end > h->H || row_begin >= row_end)
     return fail(FBS_E_ARG, "fbs_compute_rows: need 0 <= row_begin < row_end <= H");
-  return run_rows(h, left, right, row_begin, row_end, disp_band, nullptr, nullptr, nullptr, nullptr,
-                  (cudaStream_t)stream);
+  return run_rows(h, left, right, row_begin, row_end, disp_band, nullptr, nullptr, (cudaStream_t)stream);
 }
 
 extern "C" int fbs_compute_batch(fbs_ctx* h, const uint8_t* left, const uint8_t* right, int n,
@@ -257,7 +250,7 @@ extern "C" int fbs_compute_batch(fbs_ctx* h, const uint8_t* left, const uint8_t*
   int launches = 0;
   for (int i = 0; i < n; ++i) {
     int rc = run_rows(h, left + i * npix, right + i * npix, 0, h->H, disp_out + i * npix, nullptr,
-                      nullptr, nullptr, nullptr, (cudaStream_t)stream);
+                      nullptr, (cudaStream_t)stream);
     if (rc != FBS_OK) return rc;
     launches += h->launches;
   }
@@ -292,10 +285,10 @@ extern "C" int fbs_debug_volumes(fbs_ctx* h, const uint8_t* left, const uint8_t*
   const size_t npix = (size_t)h->W * h->H;
   float* tmp = nullptr;
   if (cudaMalloc(&tmp, npix * 4) != cudaSuccess) return fail(FBS_E_OOM, "fbs_debug_volumes: scratch");
-  int rc = run_rows(h, left, right, 0, h->H, tmp, nullptr, nullptr, agg_l, agg_r, s);
+  int rc = run_rows(h, left, right, 0, h->H, tmp, agg_l, agg_r, s);
   if (rc == FBS_OK) {
-    if (cost_l) k_export_vol<<<1184, 256, 0, s>>>(h->volL, h->W, h->H, h->D, h->Dp, h->Wv, h->R, cost_l);
-    if (cost_r) k_export_vol<<<1184, 256, 0, s>>>(h->volR, h->W, h->H, h->D, h->Dp, h->Wv, h->R, cost_r);
+    if (cost_l) k_export_vol<<<1184, 256, 0, s>>>(h->volL, h->W, h->H, h->D, h->nblk, h->Wv, h->R, cost_l);
+    if (cost_r) k_export_vol<<<1184, 256, 0, s>>>(h->volR, h->W, h->H, h->D, h->nblk, h->Wv, h->R, cost_r);
     rc = cuda_check(cudaGetLastError(), "fbs_debug_volumes export");
   }
   cudaStreamSynchronize(s);
@@ -308,27 +301,28 @@ extern "C" int fbs_debug_select(fbs_ctx* h, const float* agg_l, const float* agg
   if (!h || !agg_l || !agg_r) return fail(FBS_E_ARG, "fbs_debug_select: NULL argument");
   cudaStream_t s = (cudaStream_t)stream;
   const size_t npix = (size_t)h->W * h->H;
-  if (!h->c3) {
-    if (cudaMalloc(&h->c3, npix * 3 * 4) != cudaSuccess || cudaMalloc(&h->dLtmp, npix * 4) != cudaSuccess) {
-      cudaGetLastError();
-      return fail(FBS_E_OOM, "fbs_debug_select: scratch");
-    }
-  }
-  int32_t* dl = disp_l ? disp_l : h->dLtmp;
-  int32_t* dr = disp_r ? disp_r : h->dR;
   const int nb = (int)((npix + 255) / 256);
-  k_select_wta<<<nb, 256, 0, s>>>(agg_r, h->W, h->H, h->D, h->d_min, dr, nullptr);
-  k_select_wta<<<nb, 256, 0, s>>>(agg_l, h->W, h->H, h->D, h->d_min, dl, h->c3);
-  if (disp_out) k_select_final<<<nb, 256, 0, s>>>(dl, dr, h->c3, h->W, h->H, h->d_min, h->d_max, disp_out);
+  k_select_wta<<<nb, 256, 0, s>>>(agg_r, h->W, h->H, h->D, h->d_min, h->dR, nullptr);
+  k_select_wta<<<nb, 256, 0, s>>>(agg_l, h->W, h->H, h->D, h->d_min, h->dL, h->c3);
+  if (disp_out) {
+    dim3 grd((h->W + 127) / 128, h->H);
+    k_finalize<<<grd, 128, 0, s>>>(h->dL, h->dR, h->c3, h->W, 0, h->H, h->d_min, h->d_max, disp_out);
+  }
+  if (disp_l) cudaMemcpyAsync(disp_l, h->dL, npix * 4, cudaMemcpyDeviceToDevice, s);
+  if (disp_r) cudaMemcpyAsync(disp_r, h->dR, npix * 4, cudaMemcpyDeviceToDevice, s);
   return cuda_check(cudaGetLastError(), "fbs_debug_select");
 }
 
 extern "C" int fbs_debug_maps(fbs_ctx* h, const uint8_t* left, const uint8_t* right, float* disp_out,
                               int32_t* disp_l, int32_t* disp_r, fbs_stream_t stream) {
   if (!h || !left || !right || !disp_out) return fail(FBS_E_ARG, "fbs_debug_maps: NULL argument");
-  int rc = run_rows(h, left, right, 0, h->H, disp_out, disp_l, disp_r, nullptr, nullptr,
-                    (cudaStream_t)stream);
-  return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t npix = (size_t)h->W * h->H;
+  int rc = run_rows(h, left, right, 0, h->H, disp_out, nullptr, nullptr, s);
+  if (rc != FBS_OK) return rc;
+  if (disp_l) cudaMemcpyAsync(disp_l, h->dL, npix * 4, cudaMemcpyDeviceToDevice, s);
+  if (disp_r) cudaMemcpyAsync(disp_r, h->dR, npix * 4, cudaMemcpyDeviceToDevice, s);
+  return cuda_check(cudaGetLastError(), "fbs_debug_maps");
 }
 
 extern "C" int fbs_stats(const fbs_ctx* h, int* launches) {
@@ -341,9 +335,9 @@ extern "C" int fbs_profile_enable(fbs_ctx* h, int n) {
   if (!h || n < 0 || n > 65536) return fail(FBS_E_ARG, "fbs_profile_enable: bad handle or n");
   prof_free(h);
   if (n == 0) return FBS_OK;
-  h->prof_ev = new (std::nothrow) cudaEvent_t[5 * n];
+  h->prof_ev = new (std::nothrow) cudaEvent_t[kEv * n];
   if (!h->prof_ev) return fail(FBS_E_OOM, "fbs_profile_enable: host allocation");
-  for (int i = 0; i < 5 * n; ++i)
+  for (int i = 0; i < kEv * n; ++i)
     if (cudaEventCreate(&h->prof_ev[i]) != cudaSuccess) {
       for (int j = 0; j < i; ++j) cudaEventDestroy(h->prof_ev[j]);
       delete[] h->prof_ev;
@@ -359,8 +353,8 @@ extern "C" int fbs_profile_read(fbs_ctx* h, double* stage_ms, int* ncalls) {
   if (!h || !stage_ms) return fail(FBS_E_ARG, "fbs_profile_read: NULL argument");
   for (int k = 0; k < FBS_NSTAGES; ++k) stage_ms[k] = 0.0;
   for (int i = 0; i < h->prof_n; ++i) {
-    cudaEvent_t* ev = h->prof_ev + 5 * i;
-    if (cudaEventSynchronize(ev[4]) != cudaSuccess) return cuda_check(cudaGetLastError(), "fbs_profile_read");
+    cudaEvent_t* ev = h->prof_ev + kEv * i;
+    if (cudaEventSynchronize(ev[FBS_NSTAGES]) != cudaSuccess) return cuda_check(cudaGetLastError(), "fbs_profile_read");
     for (int k = 0; k < FBS_NSTAGES; ++k) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
@@ -369,5 +363,16 @@ extern "C" int fbs_profile_read(fbs_ctx* h, double* stage_ms, int* ncalls) {
   }
   if (ncalls) *ncalls = h->prof_n;
   h->prof_n = 0;
+  return FBS_OK;
+}
+
+extern "C" int fbs_tile_stats(fbs_ctx* h, long long* fast, long long* slow) {
+  if (!h) return fail(FBS_E_ARG, "fbs_tile_stats: NULL handle");
+  unsigned long long v[2] = {0, 0};
+  int rc = cuda_check(cudaMemcpy(v, h->tile_stats, sizeof(v), cudaMemcpyDeviceToHost), "fbs_tile_stats");
+  if (rc != FBS_OK) return rc;
+  cudaMemset(h->tile_stats, 0, sizeof(v));
+  if (fast) *fast = (long long)v[0];
+  if (slow) *slow = (long long)v[1];
   return FBS_OK;
 }

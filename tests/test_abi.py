@@ -43,13 +43,24 @@ def test_built_for_sm100a():
     assert "sm_100a" in out
 
 
-def test_sass_uses_ffma2():
-    """The aggregation inner loop issues FFMA2 with a broadcast scalar weight."""
+def sass_of(function: str) -> str:
     import paper_1807_02044_b200 as fbs
-    out = subprocess.run(["cuobjdump", "-sass", "-fun", "_ZN3fbs5k_aggILi0ELi4EEEvNS_7AggArgsE",
-                          fbs.LIB_PATH], capture_output=True, text=True).stdout
-    assert out.count("FFMA2") >= 100
+    out = subprocess.run(["cuobjdump", "-sass", fbs.LIB_PATH], capture_output=True, text=True).stdout
+    parts = re.split(r"\n\s*Function : ", out)
+    for p in parts:
+        if p.startswith(function):
+            return p
+    raise AssertionError(f"{function} not in the SASS of libfbs.so")
+
+
+def test_sass_uses_ffma2():
+    """The aggregation inner loop issues FFMA2 with a broadcast scalar weight
+    (the radius-4 variant: 9 taps x 4 pixels per weight row)."""
+    out = sass_of("_ZN3fbs5k_aggILi4EEEvNS_7AggArgsE")
+    assert out.count("FFMA2") >= 2592  # 32 px x 81 taps, fast path fully unrolled
     assert re.search(r"FFMA2 R\d+, R\d+\.F32, R\d+\.F32x2", out)
+    cost = sass_of("_ZN3fbs6k_costENS_8CostArgsE")
+    assert "IDP.4A" in cost or "IDP4A" in cost
 
 
 @pytest.mark.parametrize("args,code", [
