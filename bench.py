@@ -202,7 +202,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     step_ms = [a.elapsed_time(b) for a, b in ev]
     tot_ms = sum(step_ms)
     stage_ms, nprof = m.profile_read()
-    n_fast, n_slow = m.tile_stats()
+    tiles = m.tile_stats()
     m.profile_enable(0)
     t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -257,7 +257,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             "peak_source": f"148 SM x 128 FP32 lanes x 2 x {peak_src} (nominal); "
                            "FFMA2 microbenchmark 66.9 TFLOP/s (DESIGN.md §6)",
             "useful_work": "numerator FMAs of Eq.(6): 2 sides x W*H*D*(2rho+1)^2 per launch",
-            "slow_path_fraction": round(n_slow / max(1, n_fast + n_slow), 4)}
+            "denominator_forms": {k: round(v / max(1, sum(tiles.values())), 4) for k, v in tiles.items()}}
     base = None
     if world == 1 and not args.no_extras:
         base = cpu_baseline(cfg, frames_np[:1] * 3 if not banded else frames_np[:1])

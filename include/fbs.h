@@ -183,12 +183,17 @@ int fbs_profile_read(fbs_ctx* h, double* stage_ms, int* ncalls);
 
 /*
  * fbs_tile_stats — how many (CTA tile, disparity block) units of the
- * aggregation took the fast path (denominator = Σ w', d-independent) and the
- * exact slow path (explicit denominator: frame edges, textureless regions)
- * during the frames profiled since the last call (counting is on while
- * fbs_profile_enable is active).  Synchronises the device; resets the counts.
+ * aggregation took each exact form of the Eq.(6) denominator during the
+ * frames profiled since the last call (counting is on while
+ * fbs_profile_enable is active):
+ *   fast     every tap defined but the guide's own border/textureless blocks
+ *            (folded into the weights): Σ w', d-independent
+ *   edge     the frame edge cuts taps off (left pass: x-d < 1; right pass:
+ *            x+d > W-2): per-pixel prefix/suffix sums of column sums
+ *   general  textureless blocks of the other image in range: explicit sum
+ * Synchronises the device; resets the counts.  Any pointer may be NULL.
  */
-int fbs_tile_stats(fbs_ctx* h, long long* fast, long long* slow);
+int fbs_tile_stats(fbs_ctx* h, long long* fast, long long* edge, long long* general);
 
 #ifdef __cplusplus
 }

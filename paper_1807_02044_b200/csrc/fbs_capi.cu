@@ -29,10 +29,10 @@ struct fbs_ctx {
   int Wb;
   float *volL, *volR;
   int32_t *dL, *dR;
-  float4* c3;        // left WTA (c(d*), c(d*-1), c(d*+1))
+  float* aggL;       // left aggregated costs [H][nblk][W][64] (k_agg -> k_finalize)
   uint8_t *hL, *hR;  // device staging for fbs_compute_host
   float* hOut;
-  unsigned long long* tile_stats;  // device [2], counting when prof_ev is set
+  unsigned long long* tile_stats;  // device [3] FAST/EDGE/GENERAL, counting when prof_ev is set
   int launches;
   // live profiling (fbs_profile_enable): kEv events per frame
   cudaEvent_t* prof_ev;
@@ -56,7 +56,7 @@ static int cuda_check(cudaError_t e, const char* what) {
 extern "C" const char* fbs_last_error(void) { return g_err.c_str(); }
 
 static void free_all(fbs_ctx* h) {
-  void* ptrs[] = {h->defL, h->defR, h->bitsL, h->bitsR, h->volL, h->volR, h->dL, h->dR, h->c3, h->hL, h->hR, h->hOut,
+  void* ptrs[] = {h->defL, h->defR, h->bitsL, h->bitsR, h->volL, h->volR, h->dL, h->dR, h->aggL, h->hL, h->hR, h->hOut,
                   h->tile_stats};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -115,8 +115,8 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
   ok &= cudaMalloc(&h->volR, nvol * 4) == cudaSuccess;
   ok &= cudaMalloc(&h->dL, npix * 4) == cudaSuccess;
   ok &= cudaMalloc(&h->dR, npix * 4) == cudaSuccess;
-  ok &= cudaMalloc(&h->c3, npix * sizeof(float4)) == cudaSuccess;
-  ok &= cudaMalloc(&h->tile_stats, 2 * sizeof(unsigned long long)) == cudaSuccess;
+  ok &= cudaMalloc(&h->aggL, npix * h->nblk * kDB * sizeof(float)) == cudaSuccess;
+  ok &= cudaMalloc(&h->tile_stats, 3 * sizeof(unsigned long long)) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
     free_all(h);
@@ -124,10 +124,10 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
     fail(FBS_E_OOM, "fbs_create: device allocation failed");
     return nullptr;
   }
-  // margins (and never-written rows) of the volumes hold SENT
-  k_fill<<<1184, 256>>>(h->volL, nvol, kSent);
-  k_fill<<<1184, 256>>>(h->volR, nvol, kSent);
-  cudaMemset(h->tile_stats, 0, 2 * sizeof(unsigned long long));
+  // margins (and never-written rows) of the volumes hold the undefined cost
+  k_fill<<<1184, 256>>>(h->volL, nvol, kUndef);
+  k_fill<<<1184, 256>>>(h->volR, nvol, kUndef);
+  cudaMemset(h->tile_stats, 0, 3 * sizeof(unsigned long long));
   cudaMemset(h->dL, 0xff, npix * 4);
   cudaMemset(h->dR, 0xff, npix * 4);
   cudaMemset(h->defL, 0, npix);
@@ -177,8 +177,8 @@ static void fill_agg_args(const fbs_ctx* h, AggArgs& a) {
   std::memcpy(a.wr, h->wr, sizeof(a.wr));
 }
 
-static void launch_agg(const fbs_ctx* h, const AggArgs& a, cudaStream_t s) {
-  dim3 grid((h->W + kTX - 1) / kTX, (a.r1 - a.r0 + kTY - 1) / kTY, 2);
+static void launch_agg(const fbs_ctx* h, const AggArgs& a, int ty1, cudaStream_t s) {
+  dim3 grid((h->W + kTX - 1) / kTX, ty1 - a.ty0, 2);
   switch (h->R) {
 #define FBS_CASE(RR) \
   case RR: k_agg<RR><<<grid, kThreads, sizeof(AggSmem<RR>), s>>>(a); break;
@@ -191,7 +191,11 @@ static void launch_agg(const fbs_ctx* h, const AggArgs& a, cudaStream_t s) {
 static int run_rows(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0, int r1, float* out,
                     float* aggL_exp, float* aggR_exp, cudaStream_t s) {
   const int W = h->W, H = h->H, R = h->R;
-  const int c0 = std::max(0, r0 - R), c1 = std::min(H, r1 + R);  // cost rows
+  // aggregation tiles are anchored at multiples of kTY in frame rows, so a
+  // pixel's denominator form never depends on the band; cost rows cover the
+  // tiles' windows (the classification reads validity masks over them too)
+  const int ty0 = r0 / kTY, ty1 = (r1 + kTY - 1) / kTY;
+  const int c0 = std::max(0, ty0 * kTY - R), c1 = std::min(H, ty1 * kTY + R);  // cost rows
   h->launches = 0;
   cudaEvent_t* ev = nullptr;
   if (h->prof_ev && h->prof_n < h->prof_cap) ev = h->prof_ev + kEv * h->prof_n++;
@@ -211,20 +215,21 @@ static int run_rows(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0, i
   if (ev) cudaEventRecord(ev[1], s);
   AggArgs a;
   fill_agg_args(h, a);
-  a.r0 = r0; a.r1 = r1;
+  a.r0 = r0; a.r1 = r1; a.ty0 = ty0;
   a.volL = h->volL; a.volR = h->volR; a.L = L; a.Rimg = Rimg; a.defL = h->defL; a.defR = h->defR;
   a.bitsL = h->bitsL; a.bitsR = h->bitsR; a.Wb = h->Wb;
-  a.dL = h->dL; a.dR = h->dR; a.c3 = h->c3; a.exportL = aggL_exp; a.exportR = aggR_exp;
+  a.dL = h->dL; a.dR = h->dR; a.aggL = h->aggL; a.exportR = aggR_exp;
   a.tile_stats = ev ? h->tile_stats : nullptr;
-  launch_agg(h, a, s);
+  launch_agg(h, a, ty1, s);
   h->launches += 1;
   if (ev) cudaEventRecord(ev[2], s);
   {
     dim3 grd((W + 127) / 128, r1 - r0);
-    k_finalize<<<grd, 128, 0, s>>>(h->dL, h->dR, h->c3, W, r0, r1, h->d_min, h->d_max, out);
+    k_finalize<<<grd, 128, 0, s>>>(h->dL, h->dR, h->aggL, h->nblk, W, r0, r1, h->d_min, h->d_max, out);
     h->launches += 1;
   }
   if (ev) cudaEventRecord(ev[3], s);
+  if (aggL_exp) k_export_agg<<<1184, 256, 0, s>>>(h->aggL, W, H, h->D, h->nblk, aggL_exp);
   return cuda_check(cudaGetLastError(), "fbs launch");
 }
 
@@ -302,11 +307,11 @@ extern "C" int fbs_debug_select(fbs_ctx* h, const float* agg_l, const float* agg
   cudaStream_t s = (cudaStream_t)stream;
   const size_t npix = (size_t)h->W * h->H;
   const int nb = (int)((npix + 255) / 256);
-  k_select_wta<<<nb, 256, 0, s>>>(agg_r, h->W, h->H, h->D, h->d_min, h->dR, nullptr);
-  k_select_wta<<<nb, 256, 0, s>>>(agg_l, h->W, h->H, h->D, h->d_min, h->dL, h->c3);
+  k_select_wta<<<nb, 256, 0, s>>>(agg_r, h->W, h->H, h->D, h->d_min, h->nblk, h->dR, nullptr);
+  k_select_wta<<<nb, 256, 0, s>>>(agg_l, h->W, h->H, h->D, h->d_min, h->nblk, h->dL, h->aggL);
   if (disp_out) {
     dim3 grd((h->W + 127) / 128, h->H);
-    k_finalize<<<grd, 128, 0, s>>>(h->dL, h->dR, h->c3, h->W, 0, h->H, h->d_min, h->d_max, disp_out);
+    k_finalize<<<grd, 128, 0, s>>>(h->dL, h->dR, h->aggL, h->nblk, h->W, 0, h->H, h->d_min, h->d_max, disp_out);
   }
   if (disp_l) cudaMemcpyAsync(disp_l, h->dL, npix * 4, cudaMemcpyDeviceToDevice, s);
   if (disp_r) cudaMemcpyAsync(disp_r, h->dR, npix * 4, cudaMemcpyDeviceToDevice, s);
@@ -366,13 +371,14 @@ extern "C" int fbs_profile_read(fbs_ctx* h, double* stage_ms, int* ncalls) {
   return FBS_OK;
 }
 
-extern "C" int fbs_tile_stats(fbs_ctx* h, long long* fast, long long* slow) {
+extern "C" int fbs_tile_stats(fbs_ctx* h, long long* fast, long long* edge, long long* general) {
   if (!h) return fail(FBS_E_ARG, "fbs_tile_stats: NULL handle");
-  unsigned long long v[2] = {0, 0};
+  unsigned long long v[3] = {0, 0, 0};
   int rc = cuda_check(cudaMemcpy(v, h->tile_stats, sizeof(v), cudaMemcpyDeviceToHost), "fbs_tile_stats");
   if (rc != FBS_OK) return rc;
   cudaMemset(h->tile_stats, 0, sizeof(v));
   if (fast) *fast = (long long)v[0];
-  if (slow) *slow = (long long)v[1];
+  if (edge) *edge = (long long)v[1];
+  if (general) *general = (long long)v[2];
   return FBS_OK;
 }

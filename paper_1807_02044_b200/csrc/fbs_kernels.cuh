@@ -30,7 +30,8 @@
 
 namespace fbs {
 
-constexpr float kSent = -2.0f;   // undefined cost / aggregated cost (R#7)
+constexpr float kSent = -2.0f;   // undefined aggregated cost / exported cost (R#7)
+constexpr float kUndef = -0.0f;  // undefined cost inside the volumes (never a defined NCC value)
 constexpr int kMaxRadius = 6;    // FBS_MAX_RADIUS
 constexpr int kDB = 64;          // disparities per block (32 lanes x 2)
 constexpr int kPX = 4;           // warp sub-tile width  (pixels)
@@ -38,11 +39,16 @@ constexpr int kPX = 4;           // warp sub-tile width  (pixels)
 #define FBS_PY 6
 #endif
 constexpr int kPY = FBS_PY;      // warp sub-tile height (pixels)
-constexpr int kNWX = 4;          // warps across a CTA tile
-constexpr int kNWY = 2;          // warps down a CTA tile
+#ifndef FBS_NWX
+#define FBS_NWX 4
+#endif
+#ifndef FBS_NWY
+#define FBS_NWY 2
+#endif
+constexpr int kNWX = FBS_NWX;    // warps across a CTA tile
+constexpr int kNWY = FBS_NWY;    // warps down a CTA tile
 constexpr int kTX = kPX * kNWX;  // CTA tile 16 x 12
 constexpr int kTY = kPY * kNWY;
-constexpr int kPYS = kPY % 4 == 0 ? 4 : 2;  // slow-path rows per pass
 constexpr int kThreads = 32 * kNWX * kNWY;
 constexpr int kTStride = 68;     // WTA transpose row stride (floats): 16B aligned, conflict-free
 constexpr int kCX = 64;          // cost kernel: pixels per CTA (multiple of 32)
@@ -149,7 +155,7 @@ __device__ __forceinline__ void cost_side(const CostArgs& a, uint4* csm) {
         const float rl = SIDE == 0 ? rsf : rof, rr = SIDE == 0 ? rof : rsf;
         float c = __fmul_rn(__fmul_rn((float)N, rl), rr);
         c = fminf(1.0f, fmaxf(-1.0f, c));  // clamp (R#8)
-        o[k] = (rsf != 0.f && rof != 0.f && di0 + k < a.D) ? c : kSent;
+        o[k] = (rsf != 0.f && rof != 0.f && di0 + k < a.D) ? c : kUndef;
       }
       *reinterpret_cast<float2*>(vp + (size_t)b * a.Wv * kDB) = make_float2(o[0], o[1]);
     }
@@ -163,13 +169,13 @@ __global__ void __launch_bounds__(256) k_cost(CostArgs a) {
   else cost_side<1>(a, csm);
 }
 
-// fill a buffer with a float value (volume margins = SENT)
+// fill a buffer with a float value (volume margins = kUndef)
 __global__ void k_fill(float* p, size_t n, float v) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     p[i] = v;
 }
 
-// padded volume -> [H][W][D] export (debug)
+// padded volume -> [H][W][D] export (debug), undefined -> kSent
 __global__ void k_export_vol(const float* __restrict__ vol, int W, int H, int D, int nblk, int Wv, int R,
                              float* __restrict__ out) {
   const size_t n = (size_t)W * H * D;
@@ -177,7 +183,8 @@ __global__ void k_export_vol(const float* __restrict__ vol, int W, int H, int D,
     const int di = (int)(i % D);
     const size_t p = i / D;
     const int x = (int)(p % W), y = (int)(p / W);
-    out[i] = vol[vol_at(y + R, di / kDB, x + R, nblk, Wv) + di % kDB];
+    const float c = vol[vol_at(y + R, di / kDB, x + R, nblk, Wv) + di % kDB];
+    out[i] = __float_as_uint(c) == 0x80000000u ? kSent : c;
   }
 }
 
@@ -200,10 +207,11 @@ __device__ __forceinline__ float finalize_pixel(int d_int, int e, float c0, floa
   return ds;
 }
 
-// rows [r0, r1): out[(y - r0)*W + x]
+// rows [r0, r1): out[(y - r0)*W + x]; aggregated costs from the left pass's
+// [H][nblk][W][64] store
 __global__ void k_finalize(const int32_t* __restrict__ dl, const int32_t* __restrict__ dr,
-                           const float4* __restrict__ c3, int W, int r0, int r1, int d_min, int d_max,
-                           float* __restrict__ out) {
+                           const float* __restrict__ aggL, int nblk, int W, int r0, int r1, int d_min,
+                           int d_max, float* __restrict__ out) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = r0 + blockIdx.y;
   if (x >= W || y >= r1) return;
@@ -211,26 +219,62 @@ __global__ void k_finalize(const int32_t* __restrict__ dl, const int32_t* __rest
   const int d = dl[p];
   int e = -1;
   if (d >= 0 && x - d >= 0) e = dr[p - d];
-  const float4 c = c3[p];
-  out[(size_t)(y - r0) * W + x] = finalize_pixel(d, e, c.x, c.y, c.z, d_min, d_max);
+  float c0 = kSent, cm = kSent, cp = kSent;
+  if (d >= 0) {
+    auto at = [&](int di) { return aggL[(((size_t)y * nblk + di / kDB) * W + x) * kDB + di % kDB]; };
+    const int di = d - d_min;
+    c0 = at(di);
+    if (d > d_min) cm = at(di - 1);
+    if (d < d_max) cp = at(di + 1);
+  }
+  out[(size_t)(y - r0) * W + x] = finalize_pixel(d, e, c0, cm, cp, d_min, d_max);
+}
+
+// left aggregated store -> [H][W][D] export (debug)
+__global__ void k_export_agg(const float* __restrict__ aggL, int W, int H, int D, int nblk,
+                             float* __restrict__ out) {
+  const size_t n = (size_t)W * H * D;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int di = (int)(i % D);
+    const size_t p = i / D;
+    const int x = (int)(p % W), y = (int)(p / W);
+    out[i] = aggL[(((size_t)y * nblk + di / kDB) * W + x) * kDB + di % kDB];
+  }
 }
 
 // ---------------------------------------------------------------------------
 // Stage 3: fused bilateral aggregation + WTA, both sides in one grid.
+//
+// Undefined costs are stored as -0.0f (a defined NCC is never -0.0: N = 0 gives
+// +0.0), so they add nothing to the numerator Σ w c whatever their weight; the
+// denominator Σ w over the defined taps is the only place validity enters.
+// Per (CTA tile, d-block) the denominator takes one of three exact forms:
+//   FAST     every tap defined but for the guide's own blocks (folded into w'):
+//            den = Σ_q w'(p,q), d-independent
+//   EDGE     additionally only the frame edge cuts taps off (x - d < 1 on the
+//            left pass, x + d > W-2 on the right): den = a per-pixel suffix /
+//            prefix sum of the window's column sums, indexed by d
+//   GENERAL  the other image has textureless blocks in range: explicit den by
+//            FFMA2 over the validity of every tap
+// Tiles are anchored at multiples of the tile size in frame coordinates, so the
+// form a pixel gets never depends on the row band being computed.
 struct AggArgs {
-  int W, H, D, d_min, d_max, nblk, Wv, r0, r1;
+  int W, H, D, d_min, d_max, nblk, Wv, r0, r1;  // output rows [r0, r1)
+  int ty0;                       // first tile row (tiles anchored at multiples of kTY)
   const float *volL, *volR;      // cost volumes (padded layout)
   const uint8_t *L, *Rimg;       // guides (Eq.(8); right image guides the right volume, R#11)
   const uint8_t *defL, *defR;    // block-defined masks
   const uint32_t *bitsL, *bitsR; // the same masks bit-packed [H][Wb]
   int Wb;
   int32_t *dL, *dR;              // WTA maps [H][W]
-  float4* c3;                    // left: (c(d*), c(d*-1), c(d*+1), -) [H][W]
-  float *exportL, *exportR;      // optional [H][W][D] aggregated volumes
-  unsigned long long* tile_stats;  // optional [2]: (fast, slow) (CTA tile, d-block) decisions
+  float* aggL;                   // left aggregated costs, [H][nblk][W][64] (read by k_finalize)
+  float* exportR;                // optional [H][W][D] right aggregated volume (debug)
+  unsigned long long* tile_stats;  // optional [3]: FAST / EDGE / GENERAL (tile, d-block) counts
   float wd[(2 * kMaxRadius + 1) * (2 * kMaxRadius + 1)];  // ω_d, Eq.(7)
   float wr[256];                                          // ω_r, Eq.(8)
 };
+
+enum { kFast = 0, kEdge = 1, kGeneral = 2 };
 
 __device__ __forceinline__ void ffma2(float2& acc, float w, float2 c) {
   unsigned long long A, B = *reinterpret_cast<unsigned long long*>(&c);
@@ -240,6 +284,8 @@ __device__ __forceinline__ void ffma2(float2& acc, float w, float2 c) {
   acc = *reinterpret_cast<float2*>(&C);
 }
 
+__device__ __forceinline__ bool is_undef(float c) { return __float_as_uint(c) == 0x80000000u; }
+
 template <int R>
 struct AggSmem {
   static constexpr int K1 = 2 * R + 1;
@@ -247,44 +293,43 @@ struct AggSmem {
   static constexpr int GW = kTX + 2 * R, GH = kTY + 2 * R;
   float w[kNWX * kNWY][WPW];                        // [warp][py][dy][dx][px]
   float rinv[kNWX * kNWY][32];                      // 1 / Σ_q w'(p,q), 0 if none
+  float cs[kNWX * kNWY][32][K1 + 1];                // EDGE: 1 / suffix (left) or prefix (right) column sums
   float lut[kLut];                                  // ω_r(|Δ|) at Δ + 255, zero tail
-  float tb[kNWX * kNWY][8 * kTStride];              // WTA transpose, 8 pixels per round
-  float bv[kNWX * kNWY][32], bcm[kNWX * kNWY][32], bcp[kNWX * kNWY][32], lastv[kNWX * kNWY][32];
-  int bd[kNWX * kNWY][32], pend[kNWX * kNWY][32];
   int g[GH * GW];                                   // 4*(i(q)+255), or 4*kGuideSent if undefined
 };
 
-// Does any tap of this CTA tile need the explicit denominator for d-block b?
-// (the other image's block at x -+ d undefined somewhere in range; conservative)
-// One 32-bit word of the bit-packed mask per thread.
+// Classify this CTA tile for d-block b (FAST / EDGE / GENERAL), conservatively:
+// EDGE if the frame edge cuts taps off, GENERAL if the other image has an
+// undefined block anywhere in the shifted range.  One mask word per thread.
 template <int R>
-__device__ __forceinline__ bool need_slow(const AggArgs& a, int side, int x0, int y0, int b) {
+__device__ __forceinline__ int classify(const AggArgs& a, int side, int x0, int y0, int b) {
   const int qy0 = max(y0 - R, 1), qy1 = min(y0 + kTY - 1 + R, a.H - 2);
   const int qx0 = max(x0 - R, 1), qx1 = min(x0 + kTX - 1 + R, a.W - 2);
   const int d_lo = a.d_min + b * kDB, d_hi = min(d_lo + kDB - 1, a.d_max);
   const uint32_t* bits = side == 0 ? a.bitsR : a.bitsL;
-  int flag = 0;
+  int edge = 0, tex = 0;
   if (qy0 <= qy1 && qx0 <= qx1) {
     int lo, hi;
-    if (side == 0) { lo = qx0 - d_hi; hi = qx1 - d_lo; flag = lo < 1; }
-    else { lo = qx0 + d_lo; hi = qx1 + d_hi; flag = hi > a.W - 2; }
-    if (!flag) {
+    if (side == 0) { lo = qx0 - d_hi; hi = qx1 - d_lo; edge = lo < 1; lo = max(lo, 1); }
+    else { lo = qx0 + d_lo; hi = qx1 + d_hi; edge = hi > a.W - 2; hi = min(hi, a.W - 2); }
+    if (lo <= hi) {
       const int w0 = lo >> 5, nw = (hi >> 5) - w0 + 1, rows = qy1 - qy0 + 1;
       for (int i = threadIdx.x; i < nw * rows; i += kThreads) {
         const int yy = qy0 + i / nw, wi = w0 + i % nw;
         uint32_t m = 0xffffffffu;
         if (wi == w0) m &= 0xffffffffu << (lo & 31);
         if (wi == (hi >> 5)) m &= 0xffffffffu >> (31 - (hi & 31));
-        flag |= (~__ldg(bits + (size_t)yy * a.Wb + wi) & m) != 0u;
+        tex |= (~__ldg(bits + (size_t)yy * a.Wb + wi) & m) != 0u;
       }
     }
   }
-  return __syncthreads_or(flag) != 0;
+  if (__syncthreads_or(tex)) return kGeneral;
+  return edge ? kEdge : kFast;
 }
 
-// One cost row r of the fast path: all tap tests are template constants, so the
+// One cost row r of the FMA stream: tap tests are template constants, so the
 // FFMA2 stream is branch- and predicate-free (template recursion guarantees the
-// unroll; a #pragma unroll over 14 rows was re-rolled by the compiler into a
+// unroll; a #pragma unroll over the rows was re-rolled by the compiler into a
 // predicated loop).
 template <int R, int NPY, int PY0, int r>
 __device__ __forceinline__ void row_fma(const float2* c, const float* __restrict__ wsm,
@@ -306,11 +351,42 @@ __device__ __forceinline__ void row_fma(const float2* c, const float* __restrict
   }
 }
 
+// One cost row r, dx-outer: column j = dx + px is first needed at dx = j - 3, so
+// each cost pair is loaded just before that step (a short sliding window of
+// registers instead of a whole double-buffered row).
+template <int R, int r>
+__device__ __forceinline__ void row_jit(const float* __restrict__ rp, const float* __restrict__ wsm,
+                                        float2 (&num)[kPY][kPX]) {
+  constexpr int K1 = 2 * R + 1;
+  constexpr int NC = kPX + 2 * R;
+  float2 c[NC];
+#pragma unroll
+  for (int j = 0; j < kPX - 1; ++j) c[j] = __ldg(reinterpret_cast<const float2*>(rp + j * kDB));
+#pragma unroll
+  for (int dx = 0; dx < K1; ++dx) {
+    c[dx + kPX - 1] = __ldg(reinterpret_cast<const float2*>(rp + (dx + kPX - 1) * kDB));
+#pragma unroll
+    for (int pyl = 0; pyl < kPY; ++pyl) {
+      const int dy = r - pyl;
+      if (dy >= 0 && dy <= 2 * R) {
+        const float4 w = reinterpret_cast<const float4*>(wsm + (pyl * K1 + dy) * K1 * kPX)[dx];
+        ffma2(num[pyl][0], w.x, c[dx + 0]);
+        ffma2(num[pyl][1], w.y, c[dx + 1]);
+        ffma2(num[pyl][2], w.z, c[dx + 2]);
+        ffma2(num[pyl][3], w.w, c[dx + 3]);
+      }
+    }
+  }
+}
+
 template <int R, int r, int NR>
 struct FastRows {
   static __device__ __forceinline__ void run(const float* __restrict__ vb, size_t rowstride,
                                              const float* __restrict__ wsm, float2 (&cn)[kPX + 2 * R],
                                              float2 (&num)[kPY][kPX]) {
+#ifdef FBS_JIT
+    row_jit<R, r>(vb + (size_t)r * rowstride, wsm, num);
+#else
     constexpr int NC = kPX + 2 * R;
     float2 c[NC];
 #pragma unroll
@@ -321,6 +397,7 @@ struct FastRows {
       for (int j = 0; j < NC; ++j) cn[j] = __ldg(reinterpret_cast<const float2*>(rp + j * kDB));
     }
     row_fma<R, kPY, 0, r>(c, wsm, num);
+#endif
     FastRows<R, r + 1, NR>::run(vb, rowstride, wsm, cn, num);
   }
 };
@@ -330,186 +407,144 @@ struct FastRows<R, NR, NR> {
                                              float2 (&)[kPY][kPX]) {}
 };
 
-// Fast path: every tap's other-image block is defined in this d-block, so the
-// denominator is the d-independent Σ w'.  Software-pipelined: row r+1's cost
-// pairs are in flight while row r is consumed.
+// Numerator Σ_q w'(p,q) c(q,d) for the whole sub-tile (undefined c = -0.0
+// contributes nothing); software-pipelined one cost row ahead.
 template <int R>
-__device__ __forceinline__ void agg_fast(const float* __restrict__ vb, size_t rowstride,
-                                         const float* __restrict__ wsm, float2 (&num)[kPY][kPX]) {
+__device__ __forceinline__ void agg_num(const float* __restrict__ vb, size_t rowstride,
+                                        const float* __restrict__ wsm, float2 (&num)[kPY][kPX]) {
   constexpr int NC = kPX + 2 * R;
 #pragma unroll
   for (int py = 0; py < kPY; ++py)
 #pragma unroll
     for (int px = 0; px < kPX; ++px) num[py][px] = make_float2(0.f, 0.f);
   float2 cn[NC];
+#ifndef FBS_JIT
 #pragma unroll
   for (int j = 0; j < NC; ++j) cn[j] = __ldg(reinterpret_cast<const float2*>(vb + j * kDB));
+#endif
   FastRows<R, 0, kPY + 2 * R>::run(vb, rowstride, wsm, cn, num);
 }
 
-// Slow path for output rows [PY0, PY0+NPY): explicit num and den (undefined
-// costs contribute 0 to both), same tap order as the fast path, so every
-// pixel gets bit-identical results on either path.
-template <int R, int PY0, int NPY>
-__device__ __forceinline__ void agg_slow(const float* __restrict__ vb, size_t rowstride,
-                                         const float* __restrict__ wsm, float2 (&num)[NPY][kPX],
-                                         float2 (&den)[NPY][kPX]) {
-  constexpr int K1 = 2 * R + 1;
-  constexpr int NC = kPX + 2 * R;
-  constexpr int NR = NPY + 2 * R;
+template <int K1>
+__device__ __forceinline__ void load_row(const float* __restrict__ rp, float2 (&c)[kPX + K1 - 1]) {
 #pragma unroll
-  for (int py = 0; py < NPY; ++py)
+  for (int j = 0; j < kPX + K1 - 1; ++j) c[j] = __ldg(reinterpret_cast<const float2*>(rp + j * kDB));
+}
+
+// acc[px] += Σ_dx w(dy, dx, px) · c[px + dx]   (one output row, one tap row)
+template <int K1>
+__device__ __forceinline__ void tap_row(const float* __restrict__ wrow, const float2 (&c)[kPX + K1 - 1],
+                                        float2 (&acc)[kPX]) {
+#pragma unroll
+  for (int dx = 0; dx < K1; ++dx) {
+    const float4 w = reinterpret_cast<const float4*>(wrow)[dx];
+    ffma2(acc[0], w.x, c[dx + 0]);
+    ffma2(acc[1], w.y, c[dx + 1]);
+    ffma2(acc[2], w.z, c[dx + 2]);
+    ffma2(acc[3], w.w, c[dx + 3]);
+  }
+}
+
+template <int K1>
+__device__ __forceinline__ void num_den_row(const float* __restrict__ wrow, const float2 (&c)[kPX + K1 - 1],
+                                            float2 (&num)[kPX], float2 (&den)[kPX]) {
+  float2 v[kPX + K1 - 1];
+#pragma unroll
+  for (int j = 0; j < kPX + K1 - 1; ++j)
+    v[j] = make_float2(is_undef(c[j].x) ? 0.f : 1.f, is_undef(c[j].y) ? 0.f : 1.f);
+  tap_row<K1>(wrow, c, num);
+  tap_row<K1>(wrow, v, den);
+}
+
+// GENERAL: explicit num and den for two output rows (wsm, vb already offset to
+// the first of them).  Cost row r feeds output row 0 at tap row r and output
+// row 1 at tap row r-1, so rows 1..2R are a uniform runtime loop (compact code
+// for a rarely taken path) and rows 0, 2R+1 its ramps.
+template <int R>
+__device__ __forceinline__ void agg_num_den2(const float* __restrict__ vb, size_t rowstride,
+                                             const float* __restrict__ wsm, float2 (&num)[2][kPX],
+                                             float2 (&den)[2][kPX]) {
+  constexpr int K1 = 2 * R + 1;
+  constexpr int NC = kPX + K1 - 1;
+  constexpr int RS = K1 * K1 * kPX;  // weights per output row
+#pragma unroll
+  for (int py = 0; py < 2; ++py)
 #pragma unroll
     for (int px = 0; px < kPX; ++px) {
       num[py][px] = make_float2(0.f, 0.f);
       den[py][px] = make_float2(0.f, 0.f);
     }
-  const float* vb0 = vb + (size_t)PY0 * rowstride;
   float2 c[NC], cn[NC];
-#pragma unroll
-  for (int j = 0; j < NC; ++j) cn[j] = __ldg(reinterpret_cast<const float2*>(vb0 + j * kDB));
-#pragma unroll
-  for (int r = 0; r < NR; ++r) {
+  load_row<K1>(vb, cn);
+#pragma unroll 1
+  for (int r = 0; r <= 2 * R + 1; ++r) {
 #pragma unroll
     for (int j = 0; j < NC; ++j) c[j] = cn[j];
-    if (r + 1 < NR) {
-      const float* rp = vb0 + (size_t)(r + 1) * rowstride;
-#pragma unroll
-      for (int j = 0; j < NC; ++j) cn[j] = __ldg(reinterpret_cast<const float2*>(rp + j * kDB));
-    }
-    float2 v[NC];
-#pragma unroll
-    for (int j = 0; j < NC; ++j) {
-      v[j].x = c[j].x == kSent ? 0.f : 1.f;
-      v[j].y = c[j].y == kSent ? 0.f : 1.f;
-      c[j].x = c[j].x == kSent ? 0.f : c[j].x;
-      c[j].y = c[j].y == kSent ? 0.f : c[j].y;
-    }
-#pragma unroll
-    for (int dx = 0; dx < K1; ++dx) {
-#pragma unroll
-      for (int pyl = 0; pyl < NPY; ++pyl) {
-        const int dy = r - pyl;
-        if (dy < 0 || dy > 2 * R) continue;
-        const float4 w = reinterpret_cast<const float4*>(wsm + ((PY0 + pyl) * K1 + dy) * K1 * kPX)[dx];
-        ffma2(num[pyl][0], w.x, c[dx + 0]);
-        ffma2(num[pyl][1], w.y, c[dx + 1]);
-        ffma2(num[pyl][2], w.z, c[dx + 2]);
-        ffma2(num[pyl][3], w.w, c[dx + 3]);
-        ffma2(den[pyl][0], w.x, v[dx + 0]);
-        ffma2(den[pyl][1], w.y, v[dx + 1]);
-        ffma2(den[pyl][2], w.z, v[dx + 2]);
-        ffma2(den[pyl][3], w.w, v[dx + 3]);
-      }
-    }
+    if (r <= 2 * R) load_row<K1>(vb + (size_t)(r + 1) * rowstride, cn);
+    if (r <= 2 * R) num_den_row<K1>(wsm + r * K1 * kPX, c, num[0], den[0]);
+    if (r >= 1) num_den_row<K1>(wsm + RS + (r - 1) * K1 * kPX, c, num[1], den[1]);
   }
 }
 
-// slow path over the whole sub-tile in passes of kPYS rows (register budget)
-template <int R, int P>
-__device__ __forceinline__ void slow_pass(const AggArgs& a, AggSmem<R>& sm, float* exp_out, const float* vb,
-                                          size_t rowstride, int warp, int lane, int b, int sx, int sy);
+// 1/x for x > 0: MUFU reciprocal + one Newton step (<= 1 ulp; no slow path)
+__device__ __forceinline__ float rcp_nr(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return __fmul_rn(r, __fmaf_rn(-x, r, 2.0f));
+}
 
-// WTA over one 8-pixel round (2 sub-tile rows): transpose through shared memory,
-// each pixel scanned by 4 lanes x 16 d, combined with xor shuffles.
-// Strictly-greater updates in ascending d => ties go to the smallest d (R#15).
+// Order-preserving map float -> u32 (larger float <=> larger key).
+__device__ __forceinline__ unsigned fkey(float v) {
+  const unsigned b = __float_as_uint(v);
+  return b ^ ((unsigned)((int)b >> 31) | 0x80000000u);
+}
+// WTA key: aggregated value in the high word, reversed disparity index in the
+// low word, so the u64 maximum is the largest value and, among equal values,
+// the smallest d (ties -> smallest d, R#15).  0 = padded disparity slot.
+__device__ __forceinline__ unsigned long long wkey(float v, int di, int D) {
+  return di < D ? ((unsigned long long)fkey(v) << 32) | (unsigned)(0xffff - di) : 0ull;
+}
+__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) {
+  return a > b ? a : b;
+}
+__device__ __forceinline__ unsigned long long shfl_xor64(unsigned long long v, int m) {
+  const unsigned lo = __shfl_xor_sync(0xffffffffu, (unsigned)v, m);
+  const unsigned hi = __shfl_xor_sync(0xffffffffu, (unsigned)(v >> 32), m);
+  return ((unsigned long long)hi << 32) | lo;
+}
+
+// Argmax of the warp's 32 pixel slots over one d-block.  k[p] is this lane's
+// best key for pixel p.  Transposing butterfly: at each exchange a lane keeps
+// the half of its pixels selected by its lane bit, so 16+8+4+2+1 = 31 u64
+// shuffles reduce all pixels and lane l ends up holding pixel l.
+__device__ __forceinline__ unsigned long long wta_butterfly(unsigned long long (&k)[32], int lane) {
+#pragma unroll
+  for (int lvl = 0; lvl < 5; ++lvl) {
+    const int n = 16 >> lvl;
+    const bool up = lane & n;
+#pragma unroll
+    for (int i = 0; i < n; ++i) {
+      const unsigned long long keep = up ? k[n + i] : k[i];
+      const unsigned long long send = up ? k[i] : k[n + i];
+      k[i] = umax64(keep, shfl_xor64(send, n));
+    }
+  }
+  return k[0];
+}
+
+// grid: (ceil(W/kTX), tile rows, 2 sides); block 256 (8 warps, each a kPX x kPY sub-tile)
+#ifndef FBS_MINB
+#define FBS_MINB 2
+#endif
 template <int R>
-__device__ __forceinline__ void wta_round(const AggArgs& a, AggSmem<R>& sm, float* exp_out, int warp,
-                                          int lane, int b, int pyrow0, const float2 (&agg)[2][kPX],
-                                          int sx, int sy) {
-  float* tb = sm.tb[warp];
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int px = 0; px < kPX; ++px)
-      *reinterpret_cast<float2*>(tb + (i * kPX + px) * kTStride + 2 * lane) = agg[i][px];
-  __syncwarp();
-  const int j = lane >> 2, qq = lane & 3;
-  const float* row = tb + j * kTStride;
-  float vals[16];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const float4 t = *reinterpret_cast<const float4*>(row + 16 * qq + 4 * k);
-    vals[4 * k + 0] = t.x; vals[4 * k + 1] = t.y; vals[4 * k + 2] = t.z; vals[4 * k + 3] = t.w;
-  }
-  const int dbase = b * kDB + 16 * qq;  // disparity index (d - d_min) of vals[0]
-  float best = -INFINITY;
-  int bi = 0;
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const float v = (dbase + k < a.D) ? vals[k] : kSent;
-    vals[k] = v;
-    if (v > best) { best = v; bi = dbase + k; }
-  }
-#pragma unroll
-  for (int m = 1; m <= 2; m <<= 1) {
-    const float ob = __shfl_xor_sync(0xffffffffu, best, m);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, m);
-    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-  }
-  const int pyl = j >> 2, px = j & 3;
-  const int pix = (pyrow0 + pyl) * kPX + px;  // pixel index within the warp sub-tile
-  const int x = sx + px, y = sy + pyrow0 + pyl;
-  if (exp_out && x < a.W && y < a.r1 && y >= a.r0) {
-    float* dst = exp_out + ((size_t)y * a.W + x) * a.D;
-#pragma unroll
-    for (int k = 0; k < 16; ++k)
-      if (dbase + k < a.D) dst[dbase + k] = vals[k];
-  }
-  if (qq == 0) {
-    const int loc = bi - b * kDB;
-    const float v_b = best;
-    const float cm_b = loc > 0 ? row[loc - 1] : sm.lastv[warp][pix];
-    const float cp_b = loc < kDB - 1 ? row[loc + 1] : kSent;
-    if (b == 0) {
-      sm.bv[warp][pix] = v_b; sm.bd[warp][pix] = bi; sm.bcm[warp][pix] = loc > 0 ? cm_b : kSent;
-      sm.bcp[warp][pix] = cp_b; sm.pend[warp][pix] = (loc == kDB - 1);
-    } else {
-      if (sm.pend[warp][pix]) { sm.bcp[warp][pix] = row[0]; sm.pend[warp][pix] = 0; }
-      if (v_b > sm.bv[warp][pix]) {
-        sm.bv[warp][pix] = v_b; sm.bd[warp][pix] = bi; sm.bcm[warp][pix] = cm_b;
-        sm.bcp[warp][pix] = cp_b; sm.pend[warp][pix] = (loc == kDB - 1);
-      }
-    }
-    sm.lastv[warp][pix] = row[kDB - 1];
-  }
-  __syncwarp();
-}
-
-__device__ __forceinline__ void to_agg(const float2& num, const float2& den, float2& out) {
-  out.x = den.x > 0.f ? __fmul_rn(num.x, __fdiv_rn(1.0f, den.x)) : kSent;
-  out.y = den.y > 0.f ? __fmul_rn(num.y, __fdiv_rn(1.0f, den.y)) : kSent;
-}
-
-template <int R, int P>
-__device__ __forceinline__ void slow_pass(const AggArgs& a, AggSmem<R>& sm, float* exp_out, const float* vb,
-                                          size_t rowstride, int warp, int lane, int b, int sx, int sy) {
-  if constexpr (P * kPYS < kPY) {
-    float2 num[kPYS][kPX], den[kPYS][kPX];
-    agg_slow<R, P * kPYS, kPYS>(vb, rowstride, sm.w[warp], num, den);
-#pragma unroll
-    for (int rr = 0; rr < kPYS / 2; ++rr) {
-      float2 agg[2][kPX];
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int px = 0; px < kPX; ++px) to_agg(num[2 * rr + i][px], den[2 * rr + i][px], agg[i][px]);
-      wta_round<R>(a, sm, exp_out, warp, lane, b, P * kPYS + 2 * rr, agg, sx, sy);
-    }
-    slow_pass<R, P + 1>(a, sm, exp_out, vb, rowstride, warp, lane, b, sx, sy);
-  }
-}
-
-// grid: (ceil(W/kTX), ceil((r1-r0)/kTY), 2 sides); block 256 (8 warps, each a kPX x kPY sub-tile)
-template <int R>
-__global__ void __launch_bounds__(kThreads, (R <= 4) ? 2 : 1) k_agg(const AggArgs a) {
+__global__ void __launch_bounds__(kThreads, (R <= 4) ? FBS_MINB : 1) k_agg(const AggArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   AggSmem<R>& sm = *reinterpret_cast<AggSmem<R>*>(smraw);
   constexpr int K1 = 2 * R + 1;
   constexpr int GW = AggSmem<R>::GW, GH = AggSmem<R>::GH;
   const int side = blockIdx.z;  // 0: left volume / left guide, 1: right
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int x0 = blockIdx.x * kTX, y0 = a.r0 + blockIdx.y * kTY;
+  const int x0 = blockIdx.x * kTX, y0 = (a.ty0 + blockIdx.y) * kTY;
   const int wx = (warp % kNWX) * kPX, wy = (warp / kNWX) * kPY;
   const int sx = x0 + wx, sy = y0 + wy;
   const uint8_t* guide = side == 0 ? a.L : a.Rimg;
@@ -530,8 +565,13 @@ __global__ void __launch_bounds__(kThreads, (R <= 4) ? 2 : 1) k_agg(const AggArg
   }
   __syncthreads();
 
-  // ---- weights w'(p,q) = def_self(q) · ω_d(q-p) · ω_r(|i(q) - i(p)|), Eq.(6)-(8) ----
+  // ---- weights w'(p,q) = def_self(q) · ω_d(q-p) · ω_r(|i(q) - i(p)|), Eq.(6)-(8),
+  //      their sum, and the window's column sums (EDGE denominators) ----
+#ifdef FBS_EXP_NOPRO
+  if (lane < kPX * kPY && a.W < 0) {
+#else
   if (lane < kPX * kPY) {
+#endif
     const int py = lane / kPX, px = lane % kPX;
     // pixels outside the frame get some in-frame guide value: their outputs are discarded
     const int x = min(sx + px, a.W - 1), y = min(sy + py, a.H - 1);
@@ -539,71 +579,165 @@ __global__ void __launch_bounds__(kThreads, (R <= 4) ? 2 : 1) k_agg(const AggArg
     const char* lutp = reinterpret_cast<const char*>(sm.lut) - 4 * (int)guide[(size_t)y * a.W + x];
     const int* gq = sm.g + (wy + py) * GW + (wx + px);
     float wsum = 0.f;
+    float col[K1];
 #pragma unroll
-    for (int dy = 0; dy < K1; ++dy)
+    for (int dx = 0; dx < K1; ++dx) col[dx] = 0.f;
+    // Loads of a chunk of CH tap rows are issued before any store of that chunk:
+    // the weight stores may alias the guide/LUT loads as far as ptxas can tell,
+    // so interleaving them would serialise every LDS -> LDS -> STS chain.
+    constexpr int CH = (K1 * K1 <= 64) ? K1 : (64 / K1 > 0 ? 64 / K1 : 1);
+#pragma unroll
+    for (int dy0 = 0; dy0 < K1; dy0 += CH) {
+      constexpr int NB = CH * K1;
+      int gv[NB];
+      float wv[NB];
+#pragma unroll
+      for (int t = 0; t < NB; ++t) {
+        const int dy = dy0 + t / K1, dx = t % K1;
+        gv[t] = dy < K1 ? gq[dy * GW + dx] : 0;
+      }
+#pragma unroll
+      for (int t = 0; t < NB; ++t) wv[t] = *reinterpret_cast<const float*>(lutp + gv[t]);
+#pragma unroll
+      for (int t = 0; t < NB; ++t) {
+        const int dy = dy0 + t / K1, dx = t % K1;
+        if (dy < K1) {
+          const float w = __fmul_rn(a.wd[dy * K1 + dx], wv[t]);
+          wsum = __fadd_rn(wsum, w);
+          col[dx] = __fadd_rn(col[dx], w);
+          wsm[((py * K1 + dy) * K1 + dx) * kPX + px] = w;
+        }
+      }
+    }
+    sm.rinv[warp][lane] = wsum > 0.f ? rcp_nr(wsum) : 0.f;
+    // EDGE tables hold reciprocals: left pass, taps with dx >= m defined -> 1 / suffix sum;
+    // right pass, dx < m -> 1 / prefix sum (0 when no tap is defined)
+    float* cs = sm.cs[warp][lane];
+    float acc = 0.f;
+    if (side == 0) {
+      cs[K1] = 0.f;
+#pragma unroll
+      for (int dx = K1 - 1; dx >= 0; --dx) {
+        acc = __fadd_rn(acc, col[dx]);
+        cs[dx] = acc > 0.f ? rcp_nr(acc) : 0.f;
+      }
+    } else {
+      cs[0] = 0.f;
 #pragma unroll
       for (int dx = 0; dx < K1; ++dx) {
-        const float wr = *reinterpret_cast<const float*>(lutp + gq[dy * GW + dx]);
-        const float w = __fmul_rn(a.wd[dy * K1 + dx], wr);
-        wsum = __fadd_rn(wsum, w);  // dy-major, dx-minor: the FMA loops' order
-        wsm[((py * K1 + dy) * K1 + dx) * kPX + px] = w;
+        acc = __fadd_rn(acc, col[dx]);
+        cs[dx + 1] = acc > 0.f ? rcp_nr(acc) : 0.f;
       }
-    sm.rinv[warp][lane] = wsum > 0.f ? __fdiv_rn(1.0f, wsum) : 0.f;
+    }
   }
   __syncwarp();
 
   const float* vol = side == 0 ? a.volL : a.volR;
-  float* exp_out = side == 0 ? a.exportL : a.exportR;
   const size_t rowstride = (size_t)a.nblk * a.Wv * kDB;
+  unsigned long long best = 0ull;  // lane l: running best key of sub-tile pixel l
   for (int b = 0; b < a.nblk; ++b) {
     // volume row (sy - R + r) + R = sy + r; column (sx - R + j) + R = sx + j
     const float* vb = vol + vol_at(sy, b, sx, a.nblk, a.Wv) + 2 * lane;
-    const bool slow = need_slow<R>(a, side, x0, y0, b);
-    if (a.tile_stats && threadIdx.x == 0) atomicAdd(a.tile_stats + (slow ? 1 : 0), 1ull);
-    if (!slow) {
+#if defined(FBS_EXP_ALLFAST)
+    const int cls = kFast;
+#elif defined(FBS_EXP_CLSFAST)
+    const int cls0 = classify<R>(a, side, x0, y0, b);
+    const int cls = cls0 == 7 ? kEdge : kFast;
+#elif defined(FBS_EXP_ALLEDGE)
+    const int cls = kEdge;
+#elif defined(FBS_EXP_NOGEN)
+    const int cls0 = classify<R>(a, side, x0, y0, b);
+    const int cls = cls0 == kGeneral ? kEdge : cls0;
+#else
+    const int cls = classify<R>(a, side, x0, y0, b);
+#endif
+    if (a.tile_stats && threadIdx.x == 0) atomicAdd(a.tile_stats + cls, 1ull);
+    unsigned long long k[32];
+#pragma unroll
+    for (int p = kPX * kPY; p < 32; ++p) k[p] = 0ull;
+    const int di0 = b * kDB + 2 * lane;
+    // aggregated cost pair of sub-tile pixel (py, px) -> key, left-pass store, debug export
+    auto emit = [&](int py, int px, float2 agg) {
+      const int y = sy + py, x = sx + px;
+      k[py * kPX + px] = umax64(wkey(agg.x, di0, a.D), wkey(agg.y, di0 + 1, a.D));
+#ifdef FBS_EXP_NOSTORE
+      if (false) {
+#else
+      if (side == 0) {
+#endif
+        if (x < a.W && y < a.H)
+          *reinterpret_cast<float2*>(a.aggL + (((size_t)y * a.nblk + b) * a.W + x) * kDB + 2 * lane) = agg;
+      } else if (a.exportR && x < a.W && y >= a.r0 && y < a.r1) {
+        float* er = a.exportR + ((size_t)y * a.W + x) * a.D;
+        if (di0 < a.D) er[di0] = agg.x;
+        if (di0 + 1 < a.D) er[di0 + 1] = agg.y;
+      }
+    };
+    if (cls != kGeneral) {
       float2 num[kPY][kPX];
-      agg_fast<R>(vb, rowstride, sm.w[warp], num);
+      agg_num<R>(vb, rowstride, sm.w[warp], num);
 #pragma unroll
-      for (int rr = 0; rr < kPY / 2; ++rr) {
-        float2 agg[2][kPX];
+      for (int py = 0; py < kPY; ++py)
 #pragma unroll
-        for (int i = 0; i < 2; ++i)
+        for (int px = 0; px < kPX; ++px) {
+          const int pix = py * kPX + px;
+          float2 ri;  // 1 / denominator per disparity of the pair
+          if (cls == kFast) {
+            ri = make_float2(sm.rinv[warp][pix], sm.rinv[warp][pix]);
+          } else {
+            // EDGE: defined taps are those with dx >= d + 1 + R - x (left) or dx < W-1-d+R-x (right)
+            const int x = sx + px;
+            const int d0 = a.d_min + di0;
+            const int m0 = side == 0 ? d0 + 1 + R - x : a.W - 1 - d0 + R - x;
+            const int m1 = side == 0 ? m0 + 1 : m0 - 1;
+            const float* cs = sm.cs[warp][pix];
+            ri = make_float2(cs[min(max(m0, 0), K1)], cs[min(max(m1, 0), K1)]);
+          }
+          const float2 n = num[py][px];
+          emit(py, px, make_float2(ri.x > 0.f ? __fmul_rn(n.x, ri.x) : kSent,
+                                   ri.y > 0.f ? __fmul_rn(n.y, ri.y) : kSent));
+        }
+    } else {
+      const float* wsm = sm.w[warp];
+      constexpr int RS = K1 * K1 * kPX;
+#pragma unroll
+      for (int p0 = 0; p0 < kPY; p0 += 2) {
+        float2 num[2][kPX], den[2][kPX];
+        agg_num_den2<R>(vb + (size_t)p0 * rowstride, rowstride, wsm + p0 * RS, num, den);
+#pragma unroll
+        for (int pyl = 0; pyl < 2; ++pyl)
 #pragma unroll
           for (int px = 0; px < kPX; ++px) {
-            const float ri = sm.rinv[warp][(2 * rr + i) * kPX + px];
-            const float2 n = num[2 * rr + i][px];
-            agg[i][px].x = ri > 0.f ? __fmul_rn(n.x, ri) : kSent;
-            agg[i][px].y = ri > 0.f ? __fmul_rn(n.y, ri) : kSent;
+            const float2 n = num[pyl][px], dd = den[pyl][px];
+            emit(p0 + pyl, px, make_float2(dd.x > 0.f ? __fmul_rn(n.x, rcp_nr(dd.x)) : kSent,
+                                           dd.y > 0.f ? __fmul_rn(n.y, rcp_nr(dd.y)) : kSent));
           }
-        wta_round<R>(a, sm, exp_out, warp, lane, b, 2 * rr, agg, sx, sy);
       }
-    } else {
-      slow_pass<R, 0>(a, sm, exp_out, vb, rowstride, warp, lane, b, sx, sy);
     }
+#ifdef FBS_EXP_NOWTA
+    best = umax64(best, (k[lane & 7] & 0x100000000ull) | wkey(0.5f, 1, a.D));
+#else
+    best = umax64(best, wta_butterfly(k, lane));  // earlier blocks win ties (smaller d)
+#endif
   }
 
-  // ---- epilogue: one lane per sub-tile pixel ----
+  // ---- epilogue: lane l holds sub-tile pixel l ----
   if (lane < kPX * kPY) {
     const int py = lane / kPX, px = lane % kPX;
     const int x = sx + px, y = sy + py;
-    if (x < a.W && y < a.r1) {
-      const float bv = sm.bv[warp][lane];
-      const int d_int = bv > kSent ? a.d_min + sm.bd[warp][lane] : -1;
-      const size_t pi = (size_t)y * a.W + x;
-      if (side == 1) {
-        a.dR[pi] = d_int;
-      } else {
-        a.dL[pi] = d_int;
-        a.c3[pi] = make_float4(bv, sm.bcm[warp][lane], sm.bcp[warp][lane], 0.f);
-      }
+    if (x < a.W && y >= a.r0 && y < a.r1) {
+      const bool ok = (unsigned)(best >> 32) > fkey(kSent);
+      const int d_int = ok ? a.d_min + (0xffff - (int)(best & 0xffffu)) : -1;
+      (side == 0 ? a.dL : a.dR)[(size_t)y * a.W + x] = d_int;
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// Debug select path: WTA over a given [H][W][D] volume (same rules as k_agg).
-__global__ void k_select_wta(const float* __restrict__ agg, int W, int H, int D, int d_min,
-                             int32_t* __restrict__ disp, float4* __restrict__ c3) {
+// Debug select path: WTA over a given [H][W][D] volume (same rules as k_agg);
+// the left volume is also copied into the [H][nblk][W][64] layout k_finalize reads.
+__global__ void k_select_wta(const float* __restrict__ agg, int W, int H, int D, int d_min, int nblk,
+                             int32_t* __restrict__ disp, float* __restrict__ aggL) {
   const size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (p >= (size_t)W * H) return;
   const float* col = agg + p * D;
@@ -612,9 +746,12 @@ __global__ void k_select_wta(const float* __restrict__ agg, int W, int H, int D,
   for (int k = 0; k < D; ++k) {
     const float v = col[k];
     if (v > best) { best = v; bi = k; }
+    if (aggL) {
+      const size_t y = p / W, x = p % W;
+      aggL[((y * nblk + k / kDB) * W + x) * kDB + k % kDB] = v;
+    }
   }
   disp[p] = best > kSent ? d_min + bi : -1;
-  if (c3) c3[p] = make_float4(best, bi > 0 ? col[bi - 1] : kSent, bi < D - 1 ? col[bi + 1] : kSent, 0.f);
 }
 
 }  // namespace fbs
