@@ -603,12 +603,13 @@ __global__ void __launch_bounds__(kThreads, (R <= 4) ? FBS_MINB : 1) k_agg(const
         const int dy = dy0 + t / K1, dx = t % K1;
         if (dy < K1) {
           const float w = __fmul_rn(a.wd[dy * K1 + dx], wv[t]);
-          wsum = __fadd_rn(wsum, w);
           col[dx] = __fadd_rn(col[dx], w);
           wsm[((py * K1 + dy) * K1 + dx) * kPX + px] = w;
         }
       }
     }
+#pragma unroll
+    for (int dx = 0; dx < K1; ++dx) wsum = __fadd_rn(wsum, col[dx]);  // Σ w', column-major
     sm.rinv[warp][lane] = wsum > 0.f ? rcp_nr(wsum) : 0.f;
     // EDGE tables hold reciprocals: left pass, taps with dx >= m defined -> 1 / suffix sum;
     // right pass, dx < m -> 1 / prefix sum (0 when no tap is defined)
@@ -656,10 +657,15 @@ __global__ void __launch_bounds__(kThreads, (R <= 4) ? FBS_MINB : 1) k_agg(const
 #pragma unroll
     for (int p = kPX * kPY; p < 32; ++p) k[p] = 0ull;
     const int di0 = b * kDB + 2 * lane;
+    // padded disparity slots of the last block never win: their values get -inf
+    const float pad0 = di0 < a.D ? 0.f : -INFINITY, pad1 = di0 + 1 < a.D ? 0.f : -INFINITY;
+    const unsigned lo0 = 0xffffu - di0, lo1 = 0xffffu - (di0 + 1);
     // aggregated cost pair of sub-tile pixel (py, px) -> key, left-pass store, debug export
     auto emit = [&](int py, int px, float2 agg) {
       const int y = sy + py, x = sx + px;
-      k[py * kPX + px] = umax64(wkey(agg.x, di0, a.D), wkey(agg.y, di0 + 1, a.D));
+      const float v0 = agg.x + pad0, v1 = agg.y + pad1;  // exact: adds 0 or -inf
+      const bool hi = v1 > v0;                           // equal values keep the smaller d
+      k[py * kPX + px] = ((unsigned long long)fkey(hi ? v1 : v0) << 32) | (hi ? lo1 : lo0);
 #ifdef FBS_EXP_NOSTORE
       if (false) {
 #else

@@ -1,0 +1,83 @@
+#!/usr/bin/env python
+"""Turn the ncu captures of a GPU session (gpurun_out/) into the committed
+summaries under profiles/ (round-tagged):
+
+  profiles/<tag>_launches_teddy.txt   per-kernel share of the step from the
+                                      `ncu --metrics gpu__time_duration.sum` launch list
+  profiles/<tag>_<kernel>_ncu.txt     SOL / issue / stall / DRAM summary + code regions
+  profiles/ncu_summary.json           per-launch DRAM bytes of the aggregation kernel
+                                      (bench.py's roofline "traffic")
+
+usage: python tools/make_profiles.py <tag> [gpurun_out]
+"""
+import collections
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def run(cmd):
+    return subprocess.run(cmd, capture_output=True, text=True).stdout
+
+
+def launches(path):
+    rows = [r for r in csv.reader(open(path)) if r]
+    hdr_i = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hdr = rows[hdr_i]
+    ik, iv, im = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Name")
+    per = collections.defaultdict(list)
+    for r in rows[hdr_i + 1:]:
+        if len(r) > iv and r[im] == "gpu__time_duration.sum":
+            per[r[ik].split("(")[0]].append(float(r[iv].replace(",", "")))
+    return per
+
+
+def main():
+    tag = sys.argv[1]
+    src = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out")
+    out = os.path.join(ROOT, "profiles")
+    os.makedirs(out, exist_ok=True)
+    summary = {}
+    lp = os.path.join(src, "launches_teddy.csv")
+    if os.path.exists(lp):
+        per = launches(lp)
+        ours = {k: v for k, v in per.items() if any(n in k for n in ("k_cost", "k_agg", "k_finalize"))}
+        tot = sum(sum(v) for v in ours.values())
+        lines = [f"# {tag}: ncu launch list, Teddy 450x375 D=60 rho=4 (bench.py --steps 20 --warmup 3 --no-extras)",
+                 "# gpu__time_duration.sum, --clock-control none; cold-cache, serialised: compare SHARES", ""]
+        for k, v in sorted(ours.items(), key=lambda kv: -sum(kv[1])):
+            lines.append(f"{k:50s} launches={len(v):4d} mean={sum(v) / len(v) / 1e3:9.2f} us "
+                         f"share={100 * sum(v) / tot:5.1f}%")
+        open(os.path.join(out, f"{tag}_launches_teddy.txt"), "w").write("\n".join(lines) + "\n")
+    for name, rep in (("agg", "prof_round_agg"), ("cost", "prof_round_cost"), ("finalize", "prof_round_fin")):
+        rp = os.path.join(src, rep + ".ncu-rep")
+        if not os.path.exists(rp):
+            continue
+        s = run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), rp])
+        r = run([sys.executable, os.path.join(ROOT, "tools", "ncu_regions.py"), rp, "10"])
+        open(os.path.join(out, f"{tag}_{name}_teddy_ncu.txt"), "w").write(
+            f"# {tag}: ncu --set full --clock-control none, Teddy config, one launch (both sides)\n"
+            + s + "\n# code regions by stall samples (tools/ncu_regions.py)\n" + r)
+        raw = list(csv.reader(io.StringIO(run(["ncu", "-i", rp, "--page", "raw", "--csv"]))))
+        h, v = raw[0], raw[2]
+        rd = float(v[h.index("dram__bytes_read.sum")])
+        wr = float(v[h.index("dram__bytes_write.sum")])
+        unit = raw[1][h.index("dram__bytes_read.sum")]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
+        summary.setdefault("teddy", {})[f"{name}_dram_bytes_per_launch"] = (rd + wr) * scale
+        summary["teddy"][f"{name}_duration_us"] = float(v[h.index("gpu__time_duration.sum")])
+    if summary:
+        summary["note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch from one "
+                           "ncu --set full capture (replays flush caches: cold-L2 upper bound)")
+        json.dump(summary, open(os.path.join(out, "ncu_summary.json"), "w"), indent=1)
+    print(open(os.path.join(out, f"{tag}_launches_teddy.txt")).read() if os.path.exists(
+        os.path.join(out, f"{tag}_launches_teddy.txt")) else "no launch list")
+
+
+if __name__ == "__main__":
+    main()
