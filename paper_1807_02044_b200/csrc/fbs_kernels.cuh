@@ -94,7 +94,12 @@ __device__ __forceinline__ void block_pack(const uint8_t* __restrict__ img, int 
   }
   const int V = 9 * q - s * s;
   P = make_uint4(pk[0], pk[1], pk[2], (uint32_t)s);
-  if (V > 0) rs = __fdiv_rn(1.0f, __fsqrt_rn((float)V));
+  if (V > 0) {  // V^{-1/2}: MUFU rsqrt + one Newton step (~1 ulp, no slow-path branch)
+    const float v = (float)V;  // exact: V < 2^24
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+    rs = __fmul_rn(r, __fmaf_rn(__fmul_rn(-0.5f * v, r), r, 1.5f));
+  }
 }
 
 // side 0: left volume c(x, x-d); side 1: right volume c(x'+d, x').  The same
@@ -132,32 +137,39 @@ __device__ __forceinline__ void cost_side(const CostArgs& a, uint4* csm) {
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float* vol = SIDE == 0 ? a.volL : a.volR;
-  for (int xi = warp; xi < kCX; xi += 8) {
-    const int x = x0 + xi;
-    if (x >= a.W) break;
-    const uint4 ps = sP[xi];
-    const float rsf = sR[xi];
-    float* vp = vol + vol_at(y + a.R, 0, x + a.R, a.nblk, a.Wv) + 2 * lane;
-    for (int b = 0; b < a.nblk; ++b) {
-      const int di0 = b * kDB + 2 * lane;
-      // other-image staging index of disparity index di: x -+ (d_min + di) - olo
-      const int j0 = SIDE == 0 ? xi + dspan - 1 - di0 : xi + di0;
+  // warp w: the 8 consecutive pixels x0 + 8w .. x0 + 8w + 7 (unrolled: the volume
+  // and staging addresses of the 8 are immediate offsets of one base)
+  constexpr int PPW = kCX / 8;
+  const int xw = warp * PPW;
+  float* vp = vol + vol_at(y + a.R, 0, x0 + xw + a.R, a.nblk, a.Wv) + 2 * lane;
+  const size_t bstride = (size_t)a.Wv * kDB;  // next d-block of the same pixel
+  for (int b = 0; b < a.nblk; ++b) {
+    const int di0 = b * kDB + 2 * lane;
+    const bool pad0 = di0 >= a.D, pad1 = di0 + 1 >= a.D;
+    // other-image staging index of pixel xw and disparity index di0: xw -+ (d_min + di0) - olo
+    const int j0 = SIDE == 0 ? xw + dspan - 1 - di0 : xw + di0;
+#pragma unroll
+    for (int u = 0; u < PPW; ++u) {
+      if (x0 + xw + u >= a.W) break;
+      const uint4 ps = sP[xw + u];
+      const float rsf = sR[xw + u];
       float o[2];
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
-        const int j = SIDE == 0 ? j0 - k : j0 + k;
-        const float rof = oR[j];
-        const uint4 po = oP[j];
+        const int jk = SIDE == 0 ? j0 + u - k : j0 + u + k;
+        const uint4 po = oP[jk];
+        const float rof = oR[jk];
         unsigned dot = __dp4a(ps.x, po.x, 0u);
         dot = __dp4a(ps.y, po.y, dot);
         dot = __dp4a(ps.z, po.z, dot);
         const int N = 9 * (int)dot - (int)ps.w * (int)po.w;
         const float rl = SIDE == 0 ? rsf : rof, rr = SIDE == 0 ? rof : rsf;
-        float c = __fmul_rn(__fmul_rn((float)N, rl), rr);
-        c = fminf(1.0f, fmaxf(-1.0f, c));  // clamp (R#8)
-        o[k] = (rsf != 0.f && rof != 0.f && di0 + k < a.D) ? c : kUndef;
+        const float c = fminf(1.0f, fmaxf(-1.0f, __fmul_rn(__fmul_rn((float)N, rl), rr)));  // clamp (R#8)
+        o[k] = (rsf != 0.f && rof != 0.f) ? c : kUndef;
       }
-      *reinterpret_cast<float2*>(vp + (size_t)b * a.Wv * kDB) = make_float2(o[0], o[1]);
+      if (pad0) o[0] = kUndef;  // padded disparity slots of the last block
+      if (pad1) o[1] = kUndef;
+      *reinterpret_cast<float2*>(vp + (size_t)b * bstride + u * kDB) = make_float2(o[0], o[1]);
     }
   }
 }
