@@ -343,12 +343,17 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="teddy", choices=sorted(synth.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--radius", type=int, default=None,
+                    help="override the config's aggregation radius rho (NEXT-1 sweep; paper's operating point is 6)")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the e2e and cpu_baseline legs (for profiler runs)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
     cfg = synth.CONFIGS[args.config]
+    if args.radius is not None:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, radius=args.radius)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -26,6 +26,8 @@ struct fbs_ctx {
   // scratch
   uint8_t *defL, *defR;
   uint32_t *bitsL, *bitsR;
+  int32_t *goffL, *goffR;  // guide tiles for k_agg (k_cost)
+  float* lut;              // padded signed-Δ ω_r table (kLut floats)
   int Wb;
   float *volL, *volR;
   int32_t *dL, *dR;
@@ -56,7 +58,7 @@ static int cuda_check(cudaError_t e, const char* what) {
 extern "C" const char* fbs_last_error(void) { return g_err.c_str(); }
 
 static void free_all(fbs_ctx* h) {
-  void* ptrs[] = {h->defL, h->defR, h->bitsL, h->bitsR, h->volL, h->volR, h->dL, h->dR, h->aggL, h->hL, h->hR, h->hOut,
+  void* ptrs[] = {h->goffL, h->goffR, h->lut, h->defL, h->defR, h->bitsL, h->bitsR, h->volL, h->volR, h->dL, h->dR, h->aggL, h->hL, h->hR, h->hOut,
                   h->tile_stats};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -107,6 +109,9 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
   const size_t nvol = (size_t)h->Hv * h->Wv * h->nblk * kDB;
   bool ok = true;
   h->Wb = (W + kCX - 1) / kCX * (kCX / 32);
+  ok &= cudaMalloc(&h->goffL, npix * 4) == cudaSuccess;
+  ok &= cudaMalloc(&h->goffR, npix * 4) == cudaSuccess;
+  ok &= cudaMalloc(&h->lut, kLut * sizeof(float)) == cudaSuccess;
   ok &= cudaMalloc(&h->defL, npix) == cudaSuccess;
   ok &= cudaMalloc(&h->bitsL, (size_t)H * h->Wb * 4) == cudaSuccess;
   ok &= cudaMalloc(&h->bitsR, (size_t)H * h->Wb * 4) == cudaSuccess;
@@ -128,6 +133,11 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
   k_fill<<<1184, 256>>>(h->volL, nvol, kUndef);
   k_fill<<<1184, 256>>>(h->volR, nvol, kUndef);
   cudaMemset(h->tile_stats, 0, 3 * sizeof(unsigned long long));
+  {  // ω_r(|Δ|) at index Δ + 255 for Δ in [-255, 255]; zero tail for undefined taps
+    float lut[kLut];
+    for (int i = 0; i < kLut; ++i) lut[i] = (i - 255 >= -255 && i - 255 <= 255) ? h->wr[std::abs(i - 255)] : 0.f;
+    cudaMemcpy(h->lut, lut, sizeof(lut), cudaMemcpyHostToDevice);
+  }
   cudaMemset(h->dL, 0xff, npix * 4);
   cudaMemset(h->dR, 0xff, npix * 4);
   cudaMemset(h->defL, 0, npix);
@@ -174,7 +184,8 @@ static void fill_agg_args(const fbs_ctx* h, AggArgs& a) {
   a.W = h->W; a.H = h->H; a.D = h->D; a.d_min = h->d_min; a.d_max = h->d_max;
   a.nblk = h->nblk; a.Wv = h->Wv;
   std::memcpy(a.wd, h->wd, sizeof(a.wd));
-  std::memcpy(a.wr, h->wr, sizeof(a.wr));
+  a.lut = reinterpret_cast<const float4*>(h->lut);
+  a.goffL = h->goffL; a.goffR = h->goffR;
 }
 
 static void launch_agg(const fbs_ctx* h, const AggArgs& a, int ty1, cudaStream_t s) {
@@ -206,6 +217,7 @@ static int run_rows(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0, i
     ca.r0 = c0; ca.r1 = c1;
     ca.L = L; ca.Rimg = Rimg; ca.volL = h->volL; ca.volR = h->volR; ca.defL = h->defL; ca.defR = h->defR;
     ca.bitsL = h->bitsL; ca.bitsR = h->bitsR; ca.Wb = h->Wb;
+    ca.goffL = h->goffL; ca.goffR = h->goffR;
     const int ocount = kCX + h->nblk * kDB - 1;
     const size_t smem = (size_t)(kCX + ocount) * (sizeof(uint4) + sizeof(float));
     dim3 grd((W + kCX - 1) / kCX, c1 - c0, 2);

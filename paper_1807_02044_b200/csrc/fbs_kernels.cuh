@@ -72,6 +72,7 @@ struct CostArgs {
   float *volL, *volR;
   uint8_t *defL, *defR;                         // block-defined masks (bytes), rows [r0, r1)
   uint32_t *bitsL, *bitsR;                      // the same masks bit-packed [H][Wb]
+  int32_t *goffL, *goffR;                       // k_agg guide tiles: 4*(i+255), or 4*kGuideSent if undefined
 };
 
 // Eq.(2)(3) x 81 in integers: packed rows P (i(x-1) | i(x)<<8 | i(x+1)<<16 of rows
@@ -126,7 +127,12 @@ __device__ __forceinline__ void cost_side(const CostArgs& a, uint4* csm) {
       sP[i] = P; sR[i] = rs;
       const bool ok = rs != 0.f;
       const unsigned bits = __ballot_sync(0xffffffffu, ok);  // kCX is a multiple of 32
-      if (x0 + i < a.W) (SIDE == 0 ? a.defL : a.defR)[(size_t)y * a.W + x0 + i] = ok;
+      if (x0 + i < a.W) {
+        const size_t pi = (size_t)y * a.W + x0 + i;
+        const uint8_t* img = SIDE == 0 ? a.L : a.Rimg;
+        (SIDE == 0 ? a.defL : a.defR)[pi] = ok;
+        (SIDE == 0 ? a.goffL : a.goffR)[pi] = 4 * (ok ? (int)img[pi] + 255 : kGuideSent);
+      }
       if ((i & 31) == 0 && x0 + i < a.W) (SIDE == 0 ? a.bitsL : a.bitsR)[(size_t)y * a.Wb + (x0 + i) / 32] = bits;
     } else {
       const int j = i - kCX;
@@ -282,8 +288,9 @@ struct AggArgs {
   float* aggL;                   // left aggregated costs, [H][nblk][W][64] (read by k_finalize)
   float* exportR;                // optional [H][W][D] right aggregated volume (debug)
   unsigned long long* tile_stats;  // optional [3]: FAST / EDGE / GENERAL (tile, d-block) counts
+  const int32_t *goffL, *goffR;  // guide tiles, written by k_cost
+  const float4* lut;             // ω_r(|Δ|) at Δ + 255 (Eq.(8)), zero tail, kLut floats (fbs_create)
   float wd[(2 * kMaxRadius + 1) * (2 * kMaxRadius + 1)];  // ω_d, Eq.(7)
-  float wr[256];                                          // ω_r, Eq.(8)
 };
 
 enum { kFast = 0, kEdge = 1, kGeneral = 2 };
@@ -363,42 +370,11 @@ __device__ __forceinline__ void row_fma(const float2* c, const float* __restrict
   }
 }
 
-// One cost row r, dx-outer: column j = dx + px is first needed at dx = j - 3, so
-// each cost pair is loaded just before that step (a short sliding window of
-// registers instead of a whole double-buffered row).
-template <int R, int r>
-__device__ __forceinline__ void row_jit(const float* __restrict__ rp, const float* __restrict__ wsm,
-                                        float2 (&num)[kPY][kPX]) {
-  constexpr int K1 = 2 * R + 1;
-  constexpr int NC = kPX + 2 * R;
-  float2 c[NC];
-#pragma unroll
-  for (int j = 0; j < kPX - 1; ++j) c[j] = __ldg(reinterpret_cast<const float2*>(rp + j * kDB));
-#pragma unroll
-  for (int dx = 0; dx < K1; ++dx) {
-    c[dx + kPX - 1] = __ldg(reinterpret_cast<const float2*>(rp + (dx + kPX - 1) * kDB));
-#pragma unroll
-    for (int pyl = 0; pyl < kPY; ++pyl) {
-      const int dy = r - pyl;
-      if (dy >= 0 && dy <= 2 * R) {
-        const float4 w = reinterpret_cast<const float4*>(wsm + (pyl * K1 + dy) * K1 * kPX)[dx];
-        ffma2(num[pyl][0], w.x, c[dx + 0]);
-        ffma2(num[pyl][1], w.y, c[dx + 1]);
-        ffma2(num[pyl][2], w.z, c[dx + 2]);
-        ffma2(num[pyl][3], w.w, c[dx + 3]);
-      }
-    }
-  }
-}
-
 template <int R, int r, int NR>
 struct FastRows {
   static __device__ __forceinline__ void run(const float* __restrict__ vb, size_t rowstride,
                                              const float* __restrict__ wsm, float2 (&cn)[kPX + 2 * R],
                                              float2 (&num)[kPY][kPX]) {
-#ifdef FBS_JIT
-    row_jit<R, r>(vb + (size_t)r * rowstride, wsm, num);
-#else
     constexpr int NC = kPX + 2 * R;
     float2 c[NC];
 #pragma unroll
@@ -409,7 +385,6 @@ struct FastRows {
       for (int j = 0; j < NC; ++j) cn[j] = __ldg(reinterpret_cast<const float2*>(rp + j * kDB));
     }
     row_fma<R, kPY, 0, r>(c, wsm, num);
-#endif
     FastRows<R, r + 1, NR>::run(vb, rowstride, wsm, cn, num);
   }
 };
@@ -430,10 +405,8 @@ __device__ __forceinline__ void agg_num(const float* __restrict__ vb, size_t row
 #pragma unroll
     for (int px = 0; px < kPX; ++px) num[py][px] = make_float2(0.f, 0.f);
   float2 cn[NC];
-#ifndef FBS_JIT
 #pragma unroll
   for (int j = 0; j < NC; ++j) cn[j] = __ldg(reinterpret_cast<const float2*>(vb + j * kDB));
-#endif
   FastRows<R, 0, kPY + 2 * R>::run(vb, rowstride, wsm, cn, num);
 }
 
@@ -560,30 +533,19 @@ __global__ void __launch_bounds__(kThreads, (R <= 4) ? FBS_MINB : 1) k_agg(const
   const int wx = (warp % kNWX) * kPX, wy = (warp / kNWX) * kPY;
   const int sx = x0 + wx, sy = y0 + wy;
   const uint8_t* guide = side == 0 ? a.L : a.Rimg;
-  const uint8_t* def_self = side == 0 ? a.defL : a.defR;
 
-  for (int i = threadIdx.x; i < kLut; i += kThreads) {
-    const int dlt = i - 255;
-    sm.lut[i] = (dlt >= -255 && dlt <= 255) ? a.wr[abs(dlt)] : 0.f;
-  }
+  for (int i = threadIdx.x; i < kLut / 4; i += kThreads) reinterpret_cast<float4*>(sm.lut)[i] = __ldg(a.lut + i);
+  const int32_t* goff = side == 0 ? a.goffL : a.goffR;
   for (int i = threadIdx.x; i < GH * GW; i += kThreads) {
     const int qx = x0 - R + i % GW, qy = y0 - R + i / GW;
-    int g = kGuideSent;
-    if (qx >= 0 && qx < a.W && qy >= 0 && qy < a.H) {
-      const size_t qi = (size_t)qy * a.W + qx;
-      if (def_self[qi]) g = guide[qi] + 255;
-    }
-    sm.g[i] = 4 * g;  // byte offset into sm.lut before subtracting 4*i(p)
+    sm.g[i] = (qx >= 0 && qx < a.W && qy >= 0 && qy < a.H) ? __ldg(goff + (size_t)qy * a.W + qx)
+                                                             : 4 * kGuideSent;
   }
   __syncthreads();
 
   // ---- weights w'(p,q) = def_self(q) · ω_d(q-p) · ω_r(|i(q) - i(p)|), Eq.(6)-(8),
   //      their sum, and the window's column sums (EDGE denominators) ----
-#ifdef FBS_EXP_NOPRO
-  if (lane < kPX * kPY && a.W < 0) {
-#else
   if (lane < kPX * kPY) {
-#endif
     const int py = lane / kPX, px = lane % kPX;
     // pixels outside the frame get some in-frame guide value: their outputs are discarded
     const int x = min(sx + px, a.W - 1), y = min(sy + py, a.H - 1);
@@ -651,19 +613,7 @@ __global__ void __launch_bounds__(kThreads, (R <= 4) ? FBS_MINB : 1) k_agg(const
   for (int b = 0; b < a.nblk; ++b) {
     // volume row (sy - R + r) + R = sy + r; column (sx - R + j) + R = sx + j
     const float* vb = vol + vol_at(sy, b, sx, a.nblk, a.Wv) + 2 * lane;
-#if defined(FBS_EXP_ALLFAST)
-    const int cls = kFast;
-#elif defined(FBS_EXP_CLSFAST)
-    const int cls0 = classify<R>(a, side, x0, y0, b);
-    const int cls = cls0 == 7 ? kEdge : kFast;
-#elif defined(FBS_EXP_ALLEDGE)
-    const int cls = kEdge;
-#elif defined(FBS_EXP_NOGEN)
-    const int cls0 = classify<R>(a, side, x0, y0, b);
-    const int cls = cls0 == kGeneral ? kEdge : cls0;
-#else
     const int cls = classify<R>(a, side, x0, y0, b);
-#endif
     if (a.tile_stats && threadIdx.x == 0) atomicAdd(a.tile_stats + cls, 1ull);
     unsigned long long k[32];
 #pragma unroll
@@ -678,11 +628,7 @@ __global__ void __launch_bounds__(kThreads, (R <= 4) ? FBS_MINB : 1) k_agg(const
       const float v0 = agg.x + pad0, v1 = agg.y + pad1;  // exact: adds 0 or -inf
       const bool hi = v1 > v0;                           // equal values keep the smaller d
       k[py * kPX + px] = ((unsigned long long)fkey(hi ? v1 : v0) << 32) | (hi ? lo1 : lo0);
-#ifdef FBS_EXP_NOSTORE
-      if (false) {
-#else
       if (side == 0) {
-#endif
         if (x < a.W && y < a.H)
           *reinterpret_cast<float2*>(a.aggL + (((size_t)y * a.nblk + b) * a.W + x) * kDB + 2 * lane) = agg;
       } else if (a.exportR && x < a.W && y >= a.r0 && y < a.r1) {
@@ -732,11 +678,7 @@ __global__ void __launch_bounds__(kThreads, (R <= 4) ? FBS_MINB : 1) k_agg(const
           }
       }
     }
-#ifdef FBS_EXP_NOWTA
-    best = umax64(best, (k[lane & 7] & 0x100000000ull) | wkey(0.5f, 1, a.D));
-#else
     best = umax64(best, wta_butterfly(k, lane));  // earlier blocks win ties (smaller d)
-#endif
   }
 
   // ---- epilogue: lane l holds sub-tile pixel l ----
