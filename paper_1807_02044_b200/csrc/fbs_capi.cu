@@ -94,7 +94,7 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
   h->nblk = (h->D + kDB - 1) / kDB;
   h->R = radius;
   h->Wv = (W + kTX - 1) / kTX * kTX + 2 * radius;
-  h->Hv = (H + kTY - 1) / kTY * kTY + kTY + 2 * radius;
+  h->Hv = (H + kTYMax - 1) / kTYMax * kTYMax + kTYMax + 2 * radius;
   h->sigma_s = sigma_s; h->sigma_r = sigma_r;
   cudaGetDevice(&h->device);
   // Eq.(7): ω_d(dx,dy) = exp(-(dx²+dy²)/γ_d²); Eq.(8): ω_r(Δ) = exp(-Δ²/γ_r²)  (R#10)
@@ -192,7 +192,7 @@ static void launch_agg(const fbs_ctx* h, const AggArgs& a, int ty1, cudaStream_t
   dim3 grid((h->W + kTX - 1) / kTX, ty1 - a.ty0, 2);
   switch (h->R) {
 #define FBS_CASE(RR) \
-  case RR: k_agg<RR><<<grid, kThreads, sizeof(AggSmem<RR>), s>>>(a); break;
+  case RR: k_agg<RR><<<grid, AggGeom<RR>::THREADS, sizeof(AggSmem<RR>), s>>>(a); break;
     FBS_CASE(0) FBS_CASE(1) FBS_CASE(2) FBS_CASE(3) FBS_CASE(4) FBS_CASE(5) FBS_CASE(6)
 #undef FBS_CASE
   }
@@ -202,11 +202,12 @@ static void launch_agg(const fbs_ctx* h, const AggArgs& a, int ty1, cudaStream_t
 static int run_rows(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0, int r1, float* out,
                     float* aggL_exp, float* aggR_exp, cudaStream_t s) {
   const int W = h->W, H = h->H, R = h->R;
-  // aggregation tiles are anchored at multiples of kTY in frame rows, so a
+  // aggregation tiles are anchored at multiples of the tile height in frame rows, so a
   // pixel's denominator form never depends on the band; cost rows cover the
   // tiles' windows (the classification reads validity masks over them too)
-  const int ty0 = r0 / kTY, ty1 = (r1 + kTY - 1) / kTY;
-  const int c0 = std::max(0, ty0 * kTY - R), c1 = std::min(H, ty1 * kTY + R);  // cost rows
+  const int TY = agg_tile_h(R);
+  const int ty0 = r0 / TY, ty1 = (r1 + TY - 1) / TY;
+  const int c0 = std::max(0, ty0 * TY - R), c1 = std::min(H, ty1 * TY + R);  // cost rows
   h->launches = 0;
   cudaEvent_t* ev = nullptr;
   if (h->prof_ev && h->prof_n < h->prof_cap) ev = h->prof_ev + kEv * h->prof_n++;

@@ -35,21 +35,24 @@ constexpr float kUndef = -0.0f;  // undefined cost inside the volumes (never a d
 constexpr int kMaxRadius = 6;    // FBS_MAX_RADIUS
 constexpr int kDB = 64;          // disparities per block (32 lanes x 2)
 constexpr int kPX = 4;           // warp sub-tile width  (pixels)
-#ifndef FBS_PY
-#define FBS_PY 6
-#endif
-constexpr int kPY = FBS_PY;      // warp sub-tile height (pixels)
-#ifndef FBS_NWX
-#define FBS_NWX 4
-#endif
-#ifndef FBS_NWY
-#define FBS_NWY 2
-#endif
-constexpr int kNWX = FBS_NWX;    // warps across a CTA tile
-constexpr int kNWY = FBS_NWY;    // warps down a CTA tile
-constexpr int kTX = kPX * kNWX;  // CTA tile 16 x 12
-constexpr int kTY = kPY * kNWY;
-constexpr int kThreads = 32 * kNWX * kNWY;
+constexpr int kPYMax = 6;        // warp sub-tile height (pixels) for radius <= 5
+constexpr int kNWX = 4;          // warps across a CTA tile
+constexpr int kTX = kPX * kNWX;  // CTA tile width (16)
+
+// Per-radius CTA geometry of k_agg: the weight buffers grow as (2ρ+1)², so the
+// largest radius uses one warp row (4 warps, 16x6 tiles) to keep several CTAs
+// resident per SM.
+template <int R>
+struct AggGeom {
+  static constexpr int PY = R >= 6 ? 4 : kPYMax;  // warp sub-tile height (4 x PY pixels)
+  static constexpr int NWY = 2;                   // warps down a CTA tile
+  static constexpr int NW = kNWX * NWY;
+  static constexpr int TY = PY * NWY;             // CTA tile height
+  static constexpr int THREADS = 32 * NW;
+  static constexpr int MINB = 2;                  // CTAs per SM the registers are budgeted for
+};
+constexpr int kTYMax = kPYMax * 2;                // tallest CTA tile of any radius
+__host__ __device__ constexpr int agg_tile_h(int R) { return (R >= 6 ? 4 : kPYMax) * 2; }
 constexpr int kTStride = 68;     // WTA transpose row stride (floats): 16B aligned, conflict-free
 constexpr int kCX = 64;          // cost kernel: pixels per CTA (multiple of 32)
 // Range-weight LUT indexed by Δ + 255 for Δ = i(q) - i(p) in [-255, 255]; an
@@ -278,7 +281,7 @@ __global__ void k_export_agg(const float* __restrict__ aggL, int W, int H, int D
 // form a pixel gets never depends on the row band being computed.
 struct AggArgs {
   int W, H, D, d_min, d_max, nblk, Wv, r0, r1;  // output rows [r0, r1)
-  int ty0;                       // first tile row (tiles anchored at multiples of kTY)
+  int ty0;                       // first tile row (tiles anchored at multiples of the tile height)
   const float *volL, *volR;      // cost volumes (padded layout)
   const uint8_t *L, *Rimg;       // guides (Eq.(8); right image guides the right volume, R#11)
   const uint8_t *defL, *defR;    // block-defined masks
@@ -308,11 +311,12 @@ __device__ __forceinline__ bool is_undef(float c) { return __float_as_uint(c) ==
 template <int R>
 struct AggSmem {
   static constexpr int K1 = 2 * R + 1;
-  static constexpr int WPW = kPY * K1 * K1 * kPX;   // weights per warp
-  static constexpr int GW = kTX + 2 * R, GH = kTY + 2 * R;
-  float w[kNWX * kNWY][WPW];                        // [warp][py][dy][dx][px]
-  float rinv[kNWX * kNWY][32];                      // 1 / Σ_q w'(p,q), 0 if none
-  float cs[kNWX * kNWY][32][K1 + 1];                // EDGE: 1 / suffix (left) or prefix (right) column sums
+  static constexpr int WPW = AggGeom<R>::PY * K1 * K1 * kPX;  // weights per warp
+  static constexpr int NW = AggGeom<R>::NW;
+  static constexpr int GW = kTX + 2 * R, GH = AggGeom<R>::TY + 2 * R;
+  float w[NW][WPW];                                 // [warp][py][dy][dx][px]
+  float rinv[NW][32];                               // 1 / Σ_q w'(p,q), 0 if none
+  float cs[NW][32][K1 + 1];                         // EDGE: 1 / suffix (left) or prefix (right) column sums
   float lut[kLut];                                  // ω_r(|Δ|) at Δ + 255, zero tail
   int g[GH * GW];                                   // 4*(i(q)+255), or 4*kGuideSent if undefined
 };
@@ -322,7 +326,7 @@ struct AggSmem {
 // undefined block anywhere in the shifted range.  One mask word per thread.
 template <int R>
 __device__ __forceinline__ int classify(const AggArgs& a, int side, int x0, int y0, int b) {
-  const int qy0 = max(y0 - R, 1), qy1 = min(y0 + kTY - 1 + R, a.H - 2);
+  const int qy0 = max(y0 - R, 1), qy1 = min(y0 + AggGeom<R>::TY - 1 + R, a.H - 2);
   const int qx0 = max(x0 - R, 1), qx1 = min(x0 + kTX - 1 + R, a.W - 2);
   const int d_lo = a.d_min + b * kDB, d_hi = min(d_lo + kDB - 1, a.d_max);
   const uint32_t* bits = side == 0 ? a.bitsR : a.bitsL;
@@ -333,7 +337,7 @@ __device__ __forceinline__ int classify(const AggArgs& a, int side, int x0, int 
     else { lo = qx0 + d_lo; hi = qx1 + d_hi; edge = hi > a.W - 2; hi = min(hi, a.W - 2); }
     if (lo <= hi) {
       const int w0 = lo >> 5, nw = (hi >> 5) - w0 + 1, rows = qy1 - qy0 + 1;
-      for (int i = threadIdx.x; i < nw * rows; i += kThreads) {
+      for (int i = threadIdx.x; i < nw * rows; i += AggGeom<R>::THREADS) {
         const int yy = qy0 + i / nw, wi = w0 + i % nw;
         uint32_t m = 0xffffffffu;
         if (wi == w0) m &= 0xffffffffu << (lo & 31);
@@ -374,7 +378,7 @@ template <int R, int r, int NR>
 struct FastRows {
   static __device__ __forceinline__ void run(const float* __restrict__ vb, size_t rowstride,
                                              const float* __restrict__ wsm, float2 (&cn)[kPX + 2 * R],
-                                             float2 (&num)[kPY][kPX]) {
+                                             float2 (&num)[AggGeom<R>::PY][kPX]) {
     constexpr int NC = kPX + 2 * R;
     float2 c[NC];
 #pragma unroll
@@ -384,21 +388,22 @@ struct FastRows {
 #pragma unroll
       for (int j = 0; j < NC; ++j) cn[j] = __ldg(reinterpret_cast<const float2*>(rp + j * kDB));
     }
-    row_fma<R, kPY, 0, r>(c, wsm, num);
+    row_fma<R, AggGeom<R>::PY, 0, r>(c, wsm, num);
     FastRows<R, r + 1, NR>::run(vb, rowstride, wsm, cn, num);
   }
 };
 template <int R, int NR>
 struct FastRows<R, NR, NR> {
   static __device__ __forceinline__ void run(const float*, size_t, const float*, float2 (&)[kPX + 2 * R],
-                                             float2 (&)[kPY][kPX]) {}
+                                             float2 (&)[AggGeom<R>::PY][kPX]) {}
 };
 
 // Numerator Σ_q w'(p,q) c(q,d) for the whole sub-tile (undefined c = -0.0
 // contributes nothing); software-pipelined one cost row ahead.
 template <int R>
 __device__ __forceinline__ void agg_num(const float* __restrict__ vb, size_t rowstride,
-                                        const float* __restrict__ wsm, float2 (&num)[kPY][kPX]) {
+                                        const float* __restrict__ wsm, float2 (&num)[AggGeom<R>::PY][kPX]) {
+  constexpr int kPY = AggGeom<R>::PY;
   constexpr int NC = kPX + 2 * R;
 #pragma unroll
   for (int py = 0; py < kPY; ++py)
@@ -517,12 +522,12 @@ __device__ __forceinline__ unsigned long long wta_butterfly(unsigned long long (
   return k[0];
 }
 
-// grid: (ceil(W/kTX), tile rows, 2 sides); block 256 (8 warps, each a kPX x kPY sub-tile)
-#ifndef FBS_MINB
-#define FBS_MINB 2
-#endif
+// grid: (ceil(W/kTX), tile rows, 2 sides); block AggGeom<R>::THREADS (warps of 4 x PY sub-tiles)
 template <int R>
-__global__ void __launch_bounds__(kThreads, (R <= 4) ? FBS_MINB : 1) k_agg(const AggArgs a) {
+__global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(const AggArgs a) {
+  constexpr int kPY = AggGeom<R>::PY;
+  constexpr int kTY = AggGeom<R>::TY;
+  constexpr int kThreads = AggGeom<R>::THREADS;
   extern __shared__ __align__(16) unsigned char smraw[];
   AggSmem<R>& sm = *reinterpret_cast<AggSmem<R>*>(smraw);
   constexpr int K1 = 2 * R + 1;
