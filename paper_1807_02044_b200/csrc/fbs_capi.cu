@@ -11,6 +11,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <utility>
 
 #include "../../include/fbs.h"
 #include "fbs_kernels.cuh"
@@ -188,11 +189,29 @@ static void fill_agg_args(const fbs_ctx* h, AggArgs& a) {
   a.goffL = h->goffL; a.goffR = h->goffR;
 }
 
+// Launch with programmatic stream serialization (PDL): the kernel may begin
+// while its predecessor drains; it synchronises on it with pdl_wait().
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 static void launch_agg(const fbs_ctx* h, const AggArgs& a, int ty1, cudaStream_t s) {
   dim3 grid((h->W + kTX - 1) / kTX, ty1 - a.ty0, 2);
   switch (h->R) {
 #define FBS_CASE(RR) \
-  case RR: k_agg<RR><<<grid, AggGeom<RR>::THREADS, sizeof(AggSmem<RR>), s>>>(a); break;
+  case RR: launch_pdl(k_agg<RR>, grid, dim3(AggGeom<RR>::THREADS), sizeof(AggSmem<RR>), s, a); break;
     FBS_CASE(0) FBS_CASE(1) FBS_CASE(2) FBS_CASE(3) FBS_CASE(4) FBS_CASE(5) FBS_CASE(6)
 #undef FBS_CASE
   }
@@ -238,7 +257,8 @@ static int run_rows(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0, i
   if (ev) cudaEventRecord(ev[2], s);
   {
     dim3 grd((W + 127) / 128, r1 - r0);
-    k_finalize<<<grd, 128, 0, s>>>(h->dL, h->dR, h->aggL, h->nblk, W, r0, r1, h->d_min, h->d_max, out);
+    launch_pdl(k_finalize, grd, dim3(128), 0, s, (const int32_t*)h->dL, (const int32_t*)h->dR,
+               (const float*)h->aggL, h->nblk, W, r0, r1, h->d_min, h->d_max, out);
     h->launches += 1;
   }
   if (ev) cudaEventRecord(ev[3], s);

@@ -30,6 +30,13 @@
 
 namespace fbs {
 
+// Programmatic dependent launch (sm_90+): a kernel launched with the
+// programmatic-serialization attribute may start while its predecessor in
+// the stream finishes; pdl_wait() blocks until that predecessor has completed
+// and its memory is visible, pdl_trigger() lets the successor launch early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 constexpr float kSent = -2.0f;   // undefined aggregated cost / exported cost (R#7)
 constexpr float kUndef = -0.0f;  // undefined cost inside the volumes (never a defined NCC value)
 constexpr int kMaxRadius = 6;    // FBS_MAX_RADIUS
@@ -186,6 +193,7 @@ __device__ __forceinline__ void cost_side(const CostArgs& a, uint4* csm) {
 // grid: (ceil(W/kCX), r1-r0, 2 sides); block 256 = 8 warps; warp <-> pixel, lane <-> d pair.
 __global__ void __launch_bounds__(256) k_cost(CostArgs a) {
   extern __shared__ uint4 csm[];
+  pdl_trigger();  // k_agg may be scheduled now; it waits for our results in pdl_wait()
   if (blockIdx.z == 0) cost_side<0>(a, csm);
   else cost_side<1>(a, csm);
 }
@@ -233,6 +241,7 @@ __device__ __forceinline__ float finalize_pixel(int d_int, int e, float c0, floa
 __global__ void k_finalize(const int32_t* __restrict__ dl, const int32_t* __restrict__ dr,
                            const float* __restrict__ aggL, int nblk, int W, int r0, int r1, int d_min,
                            int d_max, float* __restrict__ out) {
+  pdl_wait();  // k_agg's maps
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = r0 + blockIdx.y;
   if (x >= W || y >= r1) return;
@@ -539,7 +548,9 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
   const int sx = x0 + wx, sy = y0 + wy;
   const uint8_t* guide = side == 0 ? a.L : a.Rimg;
 
+  pdl_trigger();
   for (int i = threadIdx.x; i < kLut / 4; i += kThreads) reinterpret_cast<float4*>(sm.lut)[i] = __ldg(a.lut + i);
+  pdl_wait();  // everything below reads k_cost's outputs
   const int32_t* goff = side == 0 ? a.goffL : a.goffR;
   for (int i = threadIdx.x; i < GH * GW; i += kThreads) {
     const int qx = x0 - R + i % GW, qy = y0 - R + i / GW;
