@@ -51,7 +51,8 @@ constexpr int kTX = kPX * kNWX;  // CTA tile width (16)
 // resident per SM.
 template <int R>
 struct AggGeom {
-  static constexpr int PY = R >= 6 ? 4 : kPYMax;  // warp sub-tile height (4 x PY pixels)
+  static constexpr int HPY = R >= 6 ? 2 : 3;      // output rows per half-warp
+  static constexpr int PY = 2 * HPY;              // warp sub-tile height (4 x PY pixels)
   static constexpr int NWY = 2;                   // warps down a CTA tile
   static constexpr int NW = kNWX * NWY;
   static constexpr int TY = PY * NWY;             // CTA tile height
@@ -60,7 +61,7 @@ struct AggGeom {
 };
 constexpr int kTYMax = kPYMax * 2;                // tallest CTA tile of any radius
 __host__ __device__ constexpr int agg_tile_h(int R) { return (R >= 6 ? 4 : kPYMax) * 2; }
-constexpr int kTStride = 68;     // WTA transpose row stride (floats): 16B aligned, conflict-free
+
 constexpr int kCX = 64;          // cost kernel: pixels per CTA (multiple of 32)
 // Range-weight LUT indexed by Δ + 255 for Δ = i(q) - i(p) in [-255, 255]; an
 // undefined tap q stores kGuideSent instead of i(q) + 255, landing in the zero tail.
@@ -531,6 +532,115 @@ __device__ __forceinline__ unsigned long long wta_butterfly(unsigned long long (
   return k[0];
 }
 
+// ---- 4 disparities per lane: lanes 0-15 and 16-31 (half-warps) take the
+// upper and lower 4 x HPY halves of the warp's sub-tile; every broadcast
+// weight load then feeds 2 FFMA2 per pixel (halving the L1 wavefronts per FMA).
+
+// num[pyl][px][pair] += Σ_dx w(pyl, r - pyl, dx, px) · c[px + dx]  for cost row r
+template <int R, int NPY, int r>
+__device__ __forceinline__ void row_fma4(const float4* c, const float* __restrict__ wsm,
+                                         float2 (&num)[NPY][kPX][2]) {
+  constexpr int K1 = 2 * R + 1;
+#pragma unroll
+  for (int dx = 0; dx < K1; ++dx) {
+#pragma unroll
+    for (int pyl = 0; pyl < NPY; ++pyl) {
+      const int dy = r - pyl;
+      if (dy >= 0 && dy <= 2 * R) {
+        const float4 w = reinterpret_cast<const float4*>(wsm + (pyl * K1 + dy) * K1 * kPX)[dx];
+        const float wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int px = 0; px < kPX; ++px) {
+          const float4 cc = c[dx + px];
+          ffma2(num[pyl][px][0], wv[px], make_float2(cc.x, cc.y));
+          ffma2(num[pyl][px][1], wv[px], make_float2(cc.z, cc.w));
+        }
+      }
+    }
+  }
+}
+
+template <int R, int r, int NR, int NPY>
+struct Rows4 {
+  static __device__ __forceinline__ void run(const float* __restrict__ vb, size_t rowstride,
+                                             const float* __restrict__ wsm, float2 (&num)[NPY][kPX][2]) {
+    constexpr int NC = kPX + 2 * R;
+    float4 c[NC];
+    const float* rp = vb + (size_t)r * rowstride;
+#pragma unroll
+    for (int j = 0; j < NC; ++j) c[j] = __ldg(reinterpret_cast<const float4*>(rp + j * kDB));
+    row_fma4<R, NPY, r>(c, wsm, num);
+    Rows4<R, r + 1, NR, NPY>::run(vb, rowstride, wsm, num);
+  }
+};
+template <int R, int NR, int NPY>
+struct Rows4<R, NR, NR, NPY> {
+  static __device__ __forceinline__ void run(const float*, size_t, const float*, float2 (&)[NPY][kPX][2]) {}
+};
+
+// Numerator for the half-warp's 4 x NPY pixels (undefined c = -0.0 adds nothing).
+template <int R, int NPY>
+__device__ __forceinline__ void agg_num4(const float* __restrict__ vb, size_t rowstride,
+                                         const float* __restrict__ wsm, float2 (&num)[NPY][kPX][2]) {
+#pragma unroll
+  for (int py = 0; py < NPY; ++py)
+#pragma unroll
+    for (int px = 0; px < kPX; ++px) num[py][px][0] = num[py][px][1] = make_float2(0.f, 0.f);
+  Rows4<R, 0, NPY + 2 * R, NPY>::run(vb, rowstride, wsm, num);
+}
+
+// GENERAL: explicit num and den of one output row (wrow = its weights),
+// cost rows 0..2R of that row's window, compact runtime loop.
+template <int R>
+__device__ __forceinline__ void agg_num_den_row4(const float* __restrict__ vb, size_t rowstride,
+                                                 const float* __restrict__ wrow, float2 (&num)[kPX][2],
+                                                 float2 (&den)[kPX][2]) {
+  constexpr int K1 = 2 * R + 1;
+  constexpr int NC = kPX + 2 * R;
+#pragma unroll
+  for (int px = 0; px < kPX; ++px) num[px][0] = num[px][1] = den[px][0] = den[px][1] = make_float2(0.f, 0.f);
+#pragma unroll 1
+  for (int dy = 0; dy < K1; ++dy) {
+    float4 c[NC];
+    const float* rp = vb + (size_t)dy * rowstride;
+#pragma unroll
+    for (int j = 0; j < NC; ++j) c[j] = __ldg(reinterpret_cast<const float4*>(rp + j * kDB));
+#pragma unroll
+    for (int dx = 0; dx < K1; ++dx) {
+      const float4 w = reinterpret_cast<const float4*>(wrow + dy * K1 * kPX)[dx];
+      const float wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int px = 0; px < kPX; ++px) {
+        const float4 cc = c[dx + px];
+        const float4 vv = make_float4(is_undef(cc.x) ? 0.f : 1.f, is_undef(cc.y) ? 0.f : 1.f,
+                                      is_undef(cc.z) ? 0.f : 1.f, is_undef(cc.w) ? 0.f : 1.f);
+        ffma2(num[px][0], wv[px], make_float2(cc.x, cc.y));
+        ffma2(num[px][1], wv[px], make_float2(cc.z, cc.w));
+        ffma2(den[px][0], wv[px], make_float2(vv.x, vv.y));
+        ffma2(den[px][1], wv[px], make_float2(vv.z, vv.w));
+      }
+    }
+  }
+}
+
+// Argmax of each half-warp's 16 pixel slots (k[s] = this lane's best key of slot
+// s): a transposing butterfly within the half-warp, 8+4+2+1 = 15 u64 shuffles;
+// afterwards lane l holds slot l & 15 of its half.
+__device__ __forceinline__ unsigned long long wta_butterfly16(unsigned long long (&k)[16], int lane) {
+#pragma unroll
+  for (int lvl = 0; lvl < 4; ++lvl) {
+    const int n = 8 >> lvl;
+    const bool up = lane & n;
+#pragma unroll
+    for (int i = 0; i < n; ++i) {
+      const unsigned long long keep = up ? k[n + i] : k[i];
+      const unsigned long long send = up ? k[i] : k[n + i];
+      k[i] = umax64(keep, shfl_xor64(send, n));
+    }
+  }
+  return k[0];
+}
+
 // grid: (ceil(W/kTX), tile rows, 2 sides); block AggGeom<R>::THREADS (warps of 4 x PY sub-tiles)
 template <int R>
 __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(const AggArgs a) {
@@ -625,86 +735,102 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
 
   const float* vol = side == 0 ? a.volL : a.volR;
   const size_t rowstride = (size_t)a.nblk * a.Wv * kDB;
-  unsigned long long best = 0ull;  // lane l: running best key of sub-tile pixel l
+  constexpr int HPY = AggGeom<R>::HPY;
+  constexpr int RS = K1 * K1 * kPX;                 // weights per output row
+  const int half = lane >> 4, dq = lane & 15;       // half-warp, disparity quad within the block
+  const int py0 = half * HPY;                       // first output row of this half in the sub-tile
+  const float* wsm = sm.w[warp] + py0 * RS;
+  unsigned long long best = 0ull;  // running best key of slot (lane & 15) of this half
   for (int b = 0; b < a.nblk; ++b) {
-    // volume row (sy - R + r) + R = sy + r; column (sx - R + j) + R = sx + j
-    const float* vb = vol + vol_at(sy, b, sx, a.nblk, a.Wv) + 2 * lane;
+    // volume row (sy + py0 - R + r) + R = sy + py0 + r; column (sx - R + j) + R = sx + j
+    const float* vb = vol + vol_at(sy + py0, b, sx, a.nblk, a.Wv) + 4 * dq;
     const int cls = classify<R>(a, side, x0, y0, b);
     if (a.tile_stats && threadIdx.x == 0) atomicAdd(a.tile_stats + cls, 1ull);
-    unsigned long long k[32];
+    unsigned long long k[16];
 #pragma unroll
-    for (int p = kPX * kPY; p < 32; ++p) k[p] = 0ull;
-    const int di0 = b * kDB + 2 * lane;
+    for (int s2 = kPX * HPY; s2 < 16; ++s2) k[s2] = 0ull;
+    const int di0 = b * kDB + 4 * dq;
     // padded disparity slots of the last block never win: their values get -inf
-    const float pad0 = di0 < a.D ? 0.f : -INFINITY, pad1 = di0 + 1 < a.D ? 0.f : -INFINITY;
-    const unsigned lo0 = 0xffffu - di0, lo1 = 0xffffu - (di0 + 1);
-    // aggregated cost pair of sub-tile pixel (py, px) -> key, left-pass store, debug export
-    auto emit = [&](int py, int px, float2 agg) {
-      const int y = sy + py, x = sx + px;
-      const float v0 = agg.x + pad0, v1 = agg.y + pad1;  // exact: adds 0 or -inf
-      const bool hi = v1 > v0;                           // equal values keep the smaller d
-      k[py * kPX + px] = ((unsigned long long)fkey(hi ? v1 : v0) << 32) | (hi ? lo1 : lo0);
+    float pad[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) pad[t] = di0 + t < a.D ? 0.f : -INFINITY;
+    // aggregated costs (d = di0 .. di0+3) of half-row pixel (pyl, px) -> key, left store, export
+    auto emit = [&](int pyl, int px, float4 agg) {
+      const int y = sy + py0 + pyl, x = sx + px;
+      const float v0 = agg.x + pad[0], v1 = agg.y + pad[1], v2 = agg.z + pad[2], v3 = agg.w + pad[3];
+      const bool h01 = v1 > v0, h23 = v3 > v2;     // equal values keep the smaller d
+      const float b01 = h01 ? v1 : v0, b23 = h23 ? v3 : v2;
+      const bool h = b23 > b01;
+      const int t = h ? 2 + h23 : h01;
+      k[pyl * kPX + px] = ((unsigned long long)fkey(h ? b23 : b01) << 32) | (unsigned)(0xffff - (di0 + t));
       if (side == 0) {
         if (x < a.W && y < a.H)
-          *reinterpret_cast<float2*>(a.aggL + (((size_t)y * a.nblk + b) * a.W + x) * kDB + 2 * lane) = agg;
+          *reinterpret_cast<float4*>(a.aggL + (((size_t)y * a.nblk + b) * a.W + x) * kDB + 4 * dq) = agg;
       } else if (a.exportR && x < a.W && y >= a.r0 && y < a.r1) {
         float* er = a.exportR + ((size_t)y * a.W + x) * a.D;
-        if (di0 < a.D) er[di0] = agg.x;
-        if (di0 + 1 < a.D) er[di0 + 1] = agg.y;
+        const float av[4] = {agg.x, agg.y, agg.z, agg.w};
+#pragma unroll
+        for (int tt = 0; tt < 4; ++tt)
+          if (di0 + tt < a.D) er[di0 + tt] = av[tt];
       }
     };
     if (cls != kGeneral) {
-      float2 num[kPY][kPX];
-      agg_num<R>(vb, rowstride, sm.w[warp], num);
+      float2 num[HPY][kPX][2];
+      agg_num4<R, HPY>(vb, rowstride, wsm, num);
 #pragma unroll
-      for (int py = 0; py < kPY; ++py)
+      for (int pyl = 0; pyl < HPY; ++pyl)
 #pragma unroll
         for (int px = 0; px < kPX; ++px) {
-          const int pix = py * kPX + px;
-          float2 ri;  // 1 / denominator per disparity of the pair
+          const int pix = (py0 + pyl) * kPX + px;
+          float ri[4];  // 1 / denominator per disparity
           if (cls == kFast) {
-            ri = make_float2(sm.rinv[warp][pix], sm.rinv[warp][pix]);
+            const float r0 = sm.rinv[warp][pix];
+            ri[0] = ri[1] = ri[2] = ri[3] = r0;
           } else {
             // EDGE: defined taps are those with dx >= d + 1 + R - x (left) or dx < W-1-d+R-x (right)
             const int x = sx + px;
             const int d0 = a.d_min + di0;
-            const int m0 = side == 0 ? d0 + 1 + R - x : a.W - 1 - d0 + R - x;
-            const int m1 = side == 0 ? m0 + 1 : m0 - 1;
             const float* cs = sm.cs[warp][pix];
-            ri = make_float2(cs[min(max(m0, 0), K1)], cs[min(max(m1, 0), K1)]);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int m = side == 0 ? d0 + t + 1 + R - x : a.W - 1 - (d0 + t) + R - x;
+              ri[t] = cs[min(max(m, 0), K1)];
+            }
           }
-          const float2 n = num[py][px];
-          emit(py, px, make_float2(ri.x > 0.f ? __fmul_rn(n.x, ri.x) : kSent,
-                                   ri.y > 0.f ? __fmul_rn(n.y, ri.y) : kSent));
+          const float2 n0 = num[pyl][px][0], n1 = num[pyl][px][1];
+          emit(pyl, px, make_float4(ri[0] > 0.f ? __fmul_rn(n0.x, ri[0]) : kSent,
+                                    ri[1] > 0.f ? __fmul_rn(n0.y, ri[1]) : kSent,
+                                    ri[2] > 0.f ? __fmul_rn(n1.x, ri[2]) : kSent,
+                                    ri[3] > 0.f ? __fmul_rn(n1.y, ri[3]) : kSent));
         }
     } else {
-      const float* wsm = sm.w[warp];
-      constexpr int RS = K1 * K1 * kPX;
 #pragma unroll
-      for (int p0 = 0; p0 < kPY; p0 += 2) {
-        float2 num[2][kPX], den[2][kPX];
-        agg_num_den2<R>(vb + (size_t)p0 * rowstride, rowstride, wsm + p0 * RS, num, den);
+      for (int pyl = 0; pyl < HPY; ++pyl) {
+        float2 num[kPX][2], den[kPX][2];
+        agg_num_den_row4<R>(vb + (size_t)pyl * rowstride, rowstride, wsm + pyl * RS, num, den);
 #pragma unroll
-        for (int pyl = 0; pyl < 2; ++pyl)
-#pragma unroll
-          for (int px = 0; px < kPX; ++px) {
-            const float2 n = num[pyl][px], dd = den[pyl][px];
-            emit(p0 + pyl, px, make_float2(dd.x > 0.f ? __fmul_rn(n.x, rcp_nr(dd.x)) : kSent,
-                                           dd.y > 0.f ? __fmul_rn(n.y, rcp_nr(dd.y)) : kSent));
-          }
+        for (int px = 0; px < kPX; ++px) {
+          const float2 n0 = num[px][0], n1 = num[px][1], e0 = den[px][0], e1 = den[px][1];
+          emit(pyl, px, make_float4(e0.x > 0.f ? __fmul_rn(n0.x, rcp_nr(e0.x)) : kSent,
+                                    e0.y > 0.f ? __fmul_rn(n0.y, rcp_nr(e0.y)) : kSent,
+                                    e1.x > 0.f ? __fmul_rn(n1.x, rcp_nr(e1.x)) : kSent,
+                                    e1.y > 0.f ? __fmul_rn(n1.y, rcp_nr(e1.y)) : kSent));
+        }
       }
     }
-    best = umax64(best, wta_butterfly(k, lane));  // earlier blocks win ties (smaller d)
+    best = umax64(best, wta_butterfly16(k, lane));  // earlier blocks win ties (smaller d)
   }
 
-  // ---- epilogue: lane l holds sub-tile pixel l ----
-  if (lane < kPX * kPY) {
-    const int py = lane / kPX, px = lane % kPX;
-    const int x = sx + px, y = sy + py;
-    if (x < a.W && y >= a.r0 && y < a.r1) {
-      const bool ok = (unsigned)(best >> 32) > fkey(kSent);
-      const int d_int = ok ? a.d_min + (0xffff - (int)(best & 0xffffu)) : -1;
-      (side == 0 ? a.dL : a.dR)[(size_t)y * a.W + x] = d_int;
+  // ---- epilogue: lane l holds slot l & 15 of its half ----
+  {
+    const int s2 = lane & 15;
+    if (s2 < kPX * HPY) {
+      const int x = sx + s2 % kPX, y = sy + py0 + s2 / kPX;
+      if (x < a.W && y >= a.r0 && y < a.r1) {
+        const bool ok = (unsigned)(best >> 32) > fkey(kSent);
+        const int d_int = ok ? a.d_min + (0xffff - (int)(best & 0xffffu)) : -1;
+        (side == 0 ? a.dL : a.dR)[(size_t)y * a.W + x] = d_int;
+      }
     }
   }
 }
