@@ -560,22 +560,33 @@ __device__ __forceinline__ void row_fma4(const float4* c, const float* __restric
   }
 }
 
+// Cost rows of the stream.  The first kPX columns of row r+1 (all that its first
+// dx step needs) are loaded while row r is consumed; the rest of a row is loaded
+// at its start (registers allow no more).
 template <int R, int r, int NR, int NPY>
 struct Rows4 {
   static __device__ __forceinline__ void run(const float* __restrict__ vb, size_t rowstride,
-                                             const float* __restrict__ wsm, float2 (&num)[NPY][kPX][2]) {
+                                             const float* __restrict__ wsm, float4 (&head)[kPX],
+                                             float2 (&num)[NPY][kPX][2]) {
     constexpr int NC = kPX + 2 * R;
     float4 c[NC];
     const float* rp = vb + (size_t)r * rowstride;
 #pragma unroll
-    for (int j = 0; j < NC; ++j) c[j] = __ldg(reinterpret_cast<const float4*>(rp + j * kDB));
+    for (int j = 0; j < kPX; ++j) c[j] = head[j];
+#pragma unroll
+    for (int j = kPX; j < NC; ++j) c[j] = __ldg(reinterpret_cast<const float4*>(rp + j * kDB));
+    if constexpr (r + 1 < NR) {
+#pragma unroll
+      for (int j = 0; j < kPX; ++j) head[j] = __ldg(reinterpret_cast<const float4*>(rp + rowstride + j * kDB));
+    }
     row_fma4<R, NPY, r>(c, wsm, num);
-    Rows4<R, r + 1, NR, NPY>::run(vb, rowstride, wsm, num);
+    Rows4<R, r + 1, NR, NPY>::run(vb, rowstride, wsm, head, num);
   }
 };
 template <int R, int NR, int NPY>
 struct Rows4<R, NR, NR, NPY> {
-  static __device__ __forceinline__ void run(const float*, size_t, const float*, float2 (&)[NPY][kPX][2]) {}
+  static __device__ __forceinline__ void run(const float*, size_t, const float*, float4 (&)[kPX],
+                                             float2 (&)[NPY][kPX][2]) {}
 };
 
 // Numerator for the half-warp's 4 x NPY pixels (undefined c = -0.0 adds nothing).
@@ -586,7 +597,10 @@ __device__ __forceinline__ void agg_num4(const float* __restrict__ vb, size_t ro
   for (int py = 0; py < NPY; ++py)
 #pragma unroll
     for (int px = 0; px < kPX; ++px) num[py][px][0] = num[py][px][1] = make_float2(0.f, 0.f);
-  Rows4<R, 0, NPY + 2 * R, NPY>::run(vb, rowstride, wsm, num);
+  float4 head[kPX];
+#pragma unroll
+  for (int j = 0; j < kPX; ++j) head[j] = __ldg(reinterpret_cast<const float4*>(vb + j * kDB));
+  Rows4<R, 0, NPY + 2 * R, NPY>::run(vb, rowstride, wsm, head, num);
 }
 
 // GENERAL: explicit num and den of one output row (wrow = its weights),
