@@ -1,6 +1,7 @@
-// Ceiling of the production FMA stream (fbs::agg_num<4>): each warp repeatedly
-// aggregates one 4x6-pixel sub-tile x 64 disparities from shared-memory weights
-// and an L2-resident cost volume.  No prologue, no WTA, no classification.
+// Ceiling of the production FMA stream (fbs::agg_num4<4, 3>): each half-warp
+// repeatedly aggregates its 4x3 pixels x 64 disparities (4 per lane) from
+// shared-memory weights and an L2-resident cost volume.  No prologue, no WTA,
+// no classification.
 #include <cstdio>
 #include <cuda_runtime.h>
 #include "../../paper_1807_02044_b200/csrc/fbs_kernels.cuh"
@@ -9,20 +10,26 @@ using namespace fbs;
 template <int R>
 __global__ void __launch_bounds__(256, 2) k_stream(const float* vol, size_t rowstride, int reps, float* out) {
   constexpr int K1 = 2 * R + 1;
+  constexpr int PY = AggGeom<R>::PY, HPY = AggGeom<R>::HPY;
   extern __shared__ __align__(16) float wbuf[];
-  float (*w)[kPY * K1 * K1 * kPX] = reinterpret_cast<float (*)[kPY * K1 * K1 * kPX]>(wbuf);
+  float (*w)[PY * K1 * K1 * kPX] = reinterpret_cast<float (*)[PY * K1 * K1 * kPX]>(wbuf);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < 8 * kPY * K1 * K1 * kPX; i += 256) (&w[0][0])[i] = 1e-3f * (i % 97);
+  for (int i = threadIdx.x; i < 8 * PY * K1 * K1 * kPX; i += 256) (&w[0][0])[i] = 1e-3f * (i % 97);
   __syncthreads();
-  const float* vb = vol + (size_t)(blockIdx.x % 64) * 4 * kDB * 4 + warp * kPX * kDB + 2 * lane;
+  const int half = lane >> 4, dq = lane & 15;
+  const float* vb = vol + (size_t)(blockIdx.x % 64) * 4 * kDB * 4 + warp * kPX * kDB + half * HPY * rowstride + 4 * dq;
+  const float* ws = w[warp] + half * HPY * K1 * K1 * kPX;
   float2 acc = make_float2(0.f, 0.f);
   for (int it = 0; it < reps; ++it) {
-    float2 num[kPY][kPX];
-    agg_num<R>(vb + (it & 7) * 4 * kDB, rowstride, w[warp], num);  // not loop-invariant
+    float2 num[HPY][kPX][2];
+    agg_num4<R, HPY>(vb + (it & 7) * 4 * kDB, rowstride, ws, num);  // not loop-invariant
 #pragma unroll
-    for (int py = 0; py < kPY; ++py)
+    for (int py = 0; py < HPY; ++py)
 #pragma unroll
-      for (int px = 0; px < kPX; ++px) { acc.x += num[py][px].x; acc.y += num[py][px].y; }
+      for (int px = 0; px < kPX; ++px) {
+        acc.x += num[py][px][0].x + num[py][px][1].x;
+        acc.y += num[py][px][0].y + num[py][px][1].y;
+      }
   }
   if (acc.x == 1.2345f) out[threadIdx.x] = acc.y;
 }
@@ -34,7 +41,7 @@ int main() {
   float* vol; cudaMalloc(&vol, nvol * 4); cudaMemset(vol, 0, nvol * 4);
   float* out; cudaMalloc(&out, 4096);
   const int blocks = 148 * 2, reps = 200;
-  const size_t smem = 8 * kPY * K1 * K1 * kPX * 4;
+  const size_t smem = 8 * AggGeom<R>::PY * K1 * K1 * kPX * 4;
   cudaFuncSetAttribute(k_stream<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_stream<R><<<blocks, 256, smem>>>(vol, rowstride, 2, out);
   cudaDeviceSynchronize();
@@ -46,8 +53,8 @@ int main() {
     cudaEventRecord(b); cudaEventSynchronize(b);
     float ms; cudaEventElapsedTime(&ms, a, b); if (ms < best) best = ms;
   }
-  const double ffma2 = (double)blocks * 8 * reps * (kPX * kPY * K1 * K1);
-  printf("agg_num<4> stream: %.3f ms, %.2f FFMA2/clk/SM at 1965 MHz, %.1f TFLOP/s (%s)\n", best,
+  const double ffma2 = (double)blocks * 8 * reps * (kPX * AggGeom<R>::PY * K1 * K1);
+  printf("agg_num4<4,3> stream: %.3f ms, %.2f FFMA2/clk/SM at 1965 MHz, %.1f TFLOP/s (%s)\n", best,
          ffma2 / (best * 1e-3) / 1.965e9 / 148, ffma2 * 64 * 2 / (best * 1e-3) / 1e12,
          cudaGetErrorString(cudaGetLastError()));
   return 0;
