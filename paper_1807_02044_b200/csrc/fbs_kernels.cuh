@@ -14,16 +14,17 @@
 //    are integers < 2^24; c = (N · V_l^{-1/2}) · V_r^{-1/2} in fp32 (algebraically
 //    identical to Eq.(1)-(3); R#5).  The 3x3 dot product is three DP4A on
 //    packed 3-pixel rows.
-//  * Aggregation: lanes <-> disparity pairs (32 lanes x 2 d = 64 d per block), one
-//    FFMA2 per (output pixel, tap) with the warp-uniform weight w(p,q) = ω_d ω_r as a
-//    broadcast scalar operand (SASS: FFMA2 R, Rw.F32, Rc.F32x2).  Weights are
-//    d-independent: computed once per pixel window into shared memory and reused
-//    across every disparity block ("pre-calculated").
-//  * The d-independent validity (border / textureless block of the guide's own image)
-//    is folded into the weights; the d-dependent part (the other image's block at
-//    x -+ d) only matters near the frame edges and textureless regions, detected per
-//    (CTA tile, d-block) and handled by an exact slow path with an explicit
-//    denominator.  Both paths give bit-identical results.
+//  * Aggregation: each lane holds 4 disparities (2 FFMA2 pairs) of a 64-disparity
+//    block; the two half-warps take the upper and lower halves of the warp's
+//    pixel sub-tile.  One FFMA2 per (output pixel, tap, disparity pair) with the
+//    warp-uniform weight w(p,q) = ω_d ω_r as a broadcast scalar operand (SASS:
+//    FFMA2 R, Rw.F32, Rc.F32x2).  Weights are d-independent: computed once per
+//    pixel window into shared memory and reused across every disparity block
+//    ("pre-calculated").
+//  * Undefined costs are stored as -0.0 and drop out of the numerator; the
+//    d-independent validity (border / textureless block of the guide's own image)
+//    is folded into the weights, and per (CTA tile, d-block) the denominator takes
+//    one exact form (FAST / EDGE / GENERAL, see k_agg).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -360,132 +361,6 @@ __device__ __forceinline__ int classify(const AggArgs& a, int side, int x0, int 
   return edge ? kEdge : kFast;
 }
 
-// One cost row r of the FMA stream: tap tests are template constants, so the
-// FFMA2 stream is branch- and predicate-free (template recursion guarantees the
-// unroll; a #pragma unroll over the rows was re-rolled by the compiler into a
-// predicated loop).
-template <int R, int NPY, int PY0, int r>
-__device__ __forceinline__ void row_fma(const float2* c, const float* __restrict__ wsm,
-                                        float2 (&num)[NPY][kPX]) {
-  constexpr int K1 = 2 * R + 1;
-#pragma unroll
-  for (int dx = 0; dx < K1; ++dx) {
-#pragma unroll
-    for (int pyl = 0; pyl < NPY; ++pyl) {
-      const int dy = r - pyl;
-      if (dy >= 0 && dy <= 2 * R) {
-        const float4 w = reinterpret_cast<const float4*>(wsm + ((PY0 + pyl) * K1 + dy) * K1 * kPX)[dx];
-        ffma2(num[pyl][0], w.x, c[dx + 0]);
-        ffma2(num[pyl][1], w.y, c[dx + 1]);
-        ffma2(num[pyl][2], w.z, c[dx + 2]);
-        ffma2(num[pyl][3], w.w, c[dx + 3]);
-      }
-    }
-  }
-}
-
-template <int R, int r, int NR>
-struct FastRows {
-  static __device__ __forceinline__ void run(const float* __restrict__ vb, size_t rowstride,
-                                             const float* __restrict__ wsm, float2 (&cn)[kPX + 2 * R],
-                                             float2 (&num)[AggGeom<R>::PY][kPX]) {
-    constexpr int NC = kPX + 2 * R;
-    float2 c[NC];
-#pragma unroll
-    for (int j = 0; j < NC; ++j) c[j] = cn[j];
-    if constexpr (r + 1 < NR) {
-      const float* rp = vb + (size_t)(r + 1) * rowstride;
-#pragma unroll
-      for (int j = 0; j < NC; ++j) cn[j] = __ldg(reinterpret_cast<const float2*>(rp + j * kDB));
-    }
-    row_fma<R, AggGeom<R>::PY, 0, r>(c, wsm, num);
-    FastRows<R, r + 1, NR>::run(vb, rowstride, wsm, cn, num);
-  }
-};
-template <int R, int NR>
-struct FastRows<R, NR, NR> {
-  static __device__ __forceinline__ void run(const float*, size_t, const float*, float2 (&)[kPX + 2 * R],
-                                             float2 (&)[AggGeom<R>::PY][kPX]) {}
-};
-
-// Numerator Σ_q w'(p,q) c(q,d) for the whole sub-tile (undefined c = -0.0
-// contributes nothing); software-pipelined one cost row ahead.
-template <int R>
-__device__ __forceinline__ void agg_num(const float* __restrict__ vb, size_t rowstride,
-                                        const float* __restrict__ wsm, float2 (&num)[AggGeom<R>::PY][kPX]) {
-  constexpr int kPY = AggGeom<R>::PY;
-  constexpr int NC = kPX + 2 * R;
-#pragma unroll
-  for (int py = 0; py < kPY; ++py)
-#pragma unroll
-    for (int px = 0; px < kPX; ++px) num[py][px] = make_float2(0.f, 0.f);
-  float2 cn[NC];
-#pragma unroll
-  for (int j = 0; j < NC; ++j) cn[j] = __ldg(reinterpret_cast<const float2*>(vb + j * kDB));
-  FastRows<R, 0, kPY + 2 * R>::run(vb, rowstride, wsm, cn, num);
-}
-
-template <int K1>
-__device__ __forceinline__ void load_row(const float* __restrict__ rp, float2 (&c)[kPX + K1 - 1]) {
-#pragma unroll
-  for (int j = 0; j < kPX + K1 - 1; ++j) c[j] = __ldg(reinterpret_cast<const float2*>(rp + j * kDB));
-}
-
-// acc[px] += Σ_dx w(dy, dx, px) · c[px + dx]   (one output row, one tap row)
-template <int K1>
-__device__ __forceinline__ void tap_row(const float* __restrict__ wrow, const float2 (&c)[kPX + K1 - 1],
-                                        float2 (&acc)[kPX]) {
-#pragma unroll
-  for (int dx = 0; dx < K1; ++dx) {
-    const float4 w = reinterpret_cast<const float4*>(wrow)[dx];
-    ffma2(acc[0], w.x, c[dx + 0]);
-    ffma2(acc[1], w.y, c[dx + 1]);
-    ffma2(acc[2], w.z, c[dx + 2]);
-    ffma2(acc[3], w.w, c[dx + 3]);
-  }
-}
-
-template <int K1>
-__device__ __forceinline__ void num_den_row(const float* __restrict__ wrow, const float2 (&c)[kPX + K1 - 1],
-                                            float2 (&num)[kPX], float2 (&den)[kPX]) {
-  float2 v[kPX + K1 - 1];
-#pragma unroll
-  for (int j = 0; j < kPX + K1 - 1; ++j)
-    v[j] = make_float2(is_undef(c[j].x) ? 0.f : 1.f, is_undef(c[j].y) ? 0.f : 1.f);
-  tap_row<K1>(wrow, c, num);
-  tap_row<K1>(wrow, v, den);
-}
-
-// GENERAL: explicit num and den for two output rows (wsm, vb already offset to
-// the first of them).  Cost row r feeds output row 0 at tap row r and output
-// row 1 at tap row r-1, so rows 1..2R are a uniform runtime loop (compact code
-// for a rarely taken path) and rows 0, 2R+1 its ramps.
-template <int R>
-__device__ __forceinline__ void agg_num_den2(const float* __restrict__ vb, size_t rowstride,
-                                             const float* __restrict__ wsm, float2 (&num)[2][kPX],
-                                             float2 (&den)[2][kPX]) {
-  constexpr int K1 = 2 * R + 1;
-  constexpr int NC = kPX + K1 - 1;
-  constexpr int RS = K1 * K1 * kPX;  // weights per output row
-#pragma unroll
-  for (int py = 0; py < 2; ++py)
-#pragma unroll
-    for (int px = 0; px < kPX; ++px) {
-      num[py][px] = make_float2(0.f, 0.f);
-      den[py][px] = make_float2(0.f, 0.f);
-    }
-  float2 c[NC], cn[NC];
-  load_row<K1>(vb, cn);
-#pragma unroll 1
-  for (int r = 0; r <= 2 * R + 1; ++r) {
-#pragma unroll
-    for (int j = 0; j < NC; ++j) c[j] = cn[j];
-    if (r <= 2 * R) load_row<K1>(vb + (size_t)(r + 1) * rowstride, cn);
-    if (r <= 2 * R) num_den_row<K1>(wsm + r * K1 * kPX, c, num[0], den[0]);
-    if (r >= 1) num_den_row<K1>(wsm + RS + (r - 1) * K1 * kPX, c, num[1], den[1]);
-  }
-}
-
 // 1/x for x > 0: MUFU reciprocal + one Newton step (<= 1 ulp; no slow path)
 __device__ __forceinline__ float rcp_nr(float x) {
   float r;
@@ -498,12 +373,6 @@ __device__ __forceinline__ unsigned fkey(float v) {
   const unsigned b = __float_as_uint(v);
   return b ^ ((unsigned)((int)b >> 31) | 0x80000000u);
 }
-// WTA key: aggregated value in the high word, reversed disparity index in the
-// low word, so the u64 maximum is the largest value and, among equal values,
-// the smallest d (ties -> smallest d, R#15).  0 = padded disparity slot.
-__device__ __forceinline__ unsigned long long wkey(float v, int di, int D) {
-  return di < D ? ((unsigned long long)fkey(v) << 32) | (unsigned)(0xffff - di) : 0ull;
-}
 __device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) {
   return a > b ? a : b;
 }
@@ -511,25 +380,6 @@ __device__ __forceinline__ unsigned long long shfl_xor64(unsigned long long v, i
   const unsigned lo = __shfl_xor_sync(0xffffffffu, (unsigned)v, m);
   const unsigned hi = __shfl_xor_sync(0xffffffffu, (unsigned)(v >> 32), m);
   return ((unsigned long long)hi << 32) | lo;
-}
-
-// Argmax of the warp's 32 pixel slots over one d-block.  k[p] is this lane's
-// best key for pixel p.  Transposing butterfly: at each exchange a lane keeps
-// the half of its pixels selected by its lane bit, so 16+8+4+2+1 = 31 u64
-// shuffles reduce all pixels and lane l ends up holding pixel l.
-__device__ __forceinline__ unsigned long long wta_butterfly(unsigned long long (&k)[32], int lane) {
-#pragma unroll
-  for (int lvl = 0; lvl < 5; ++lvl) {
-    const int n = 16 >> lvl;
-    const bool up = lane & n;
-#pragma unroll
-    for (int i = 0; i < n; ++i) {
-      const unsigned long long keep = up ? k[n + i] : k[i];
-      const unsigned long long send = up ? k[i] : k[n + i];
-      k[i] = umax64(keep, shfl_xor64(send, n));
-    }
-  }
-  return k[0];
 }
 
 // ---- 4 disparities per lane: lanes 0-15 and 16-31 (half-warps) take the
