@@ -22,13 +22,13 @@ struct fbs_ctx {
   int W, H, d_min, d_max, D, nblk, R, Wv, Hv;
   float sigma_s, sigma_r;
   int device;
-  float wd[(2 * kMaxRadius + 1) * (2 * kMaxRadius + 1)];
-  float wr[256];
+  // Eq.(7)(8) in the exponent form k_agg evaluates: w' = 2^(cd(dx,dy) + nkr Δ²)
+  float cd[(2 * kMaxRadius + 1) * (2 * kMaxRadius + 1)];
+  float nkr;
   // scratch
-  uint8_t *defL, *defR;
   uint32_t *bitsL, *bitsR;
-  int32_t *goffL, *goffR;  // guide tiles for k_agg (k_cost)
-  float* lut;              // padded signed-Δ ω_r table (kLut floats)
+  float *gpadL, *gpadR;    // padded guide images for k_agg (k_cost), [guide_rows][Wg]
+  int Wg;
   int Wb;
   float *volL, *volR;
   int32_t *dL, *dR;
@@ -59,7 +59,7 @@ static int cuda_check(cudaError_t e, const char* what) {
 extern "C" const char* fbs_last_error(void) { return g_err.c_str(); }
 
 static void free_all(fbs_ctx* h) {
-  void* ptrs[] = {h->goffL, h->goffR, h->lut, h->defL, h->defR, h->bitsL, h->bitsR, h->volL, h->volR, h->dL, h->dR, h->aggL, h->hL, h->hR, h->hOut,
+  void* ptrs[] = {h->gpadL, h->gpadR, h->bitsL, h->bitsR, h->volL, h->volR, h->dL, h->dR, h->aggL, h->hL, h->hR, h->hOut,
                   h->tile_stats};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -75,6 +75,10 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
   if (d_min < 0 || d_max <= d_min || radius < 0 || !std::isfinite(sigma_s) || !(sigma_s > 0) ||
       !std::isfinite(sigma_r) || !(sigma_r > 0)) {
     fail(FBS_E_PARAM, "fbs_create: need 0 <= d_min < d_max, radius >= 0, finite sigma_s, sigma_r > 0");
+    return nullptr;
+  }
+  if (sigma_r > FBS_MAX_SIGMA_R) {
+    fail(FBS_E_UNSUPPORTED, "fbs_create: sigma_r > FBS_MAX_SIGMA_R");
     return nullptr;
   }
   if (radius > kMaxRadius) {
@@ -98,25 +102,27 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
   h->Hv = (H + kTYMax - 1) / kTYMax * kTYMax + kTYMax + 2 * radius;
   h->sigma_s = sigma_s; h->sigma_r = sigma_r;
   cudaGetDevice(&h->device);
-  // Eq.(7): ω_d(dx,dy) = exp(-(dx²+dy²)/γ_d²); Eq.(8): ω_r(Δ) = exp(-Δ²/γ_r²)  (R#10)
+  // Eq.(7): ω_d(dx,dy) = exp(-(dx²+dy²)/γ_d²); Eq.(8): ω_r(Δ) = exp(-Δ²/γ_r²)  (R#10).
+  // k_agg evaluates the product as one power of two: ω_d ω_r = 2^(cd(dx,dy) + nkr Δ²),
+  // cd = -log2(e)(dx²+dy²)/γ_d², nkr = -log2(e)/γ_r² (built in double, rounded once;
+  // P:L199 "pre-calculated").
   const int K1 = 2 * radius + 1;
-  const double gd = sigma_s, gr = sigma_r;
+  const double gd = sigma_s, gr = sigma_r, l2e = 1.4426950408889634;
   for (int dy = -radius; dy <= radius; ++dy)
     for (int dx = -radius; dx <= radius; ++dx)
-      h->wd[(dy + radius) * K1 + (dx + radius)] = (float)std::exp(-(double)(dx * dx + dy * dy) / (gd * gd));
-  for (int a = 0; a < 256; ++a) h->wr[a] = (float)std::exp(-(double)a * a / (gr * gr));
+      h->cd[(dy + radius) * K1 + (dx + radius)] = (float)(-l2e * (double)(dx * dx + dy * dy) / (gd * gd));
+  h->nkr = (float)(-l2e / (gr * gr));
 
   const size_t npix = (size_t)W * H;
   const size_t nvol = (size_t)h->Hv * h->Wv * h->nblk * kDB;
   bool ok = true;
   h->Wb = (W + kCX - 1) / kCX * (kCX / 32);
-  ok &= cudaMalloc(&h->goffL, npix * 4) == cudaSuccess;
-  ok &= cudaMalloc(&h->goffR, npix * 4) == cudaSuccess;
-  ok &= cudaMalloc(&h->lut, kLut * sizeof(float)) == cudaSuccess;
-  ok &= cudaMalloc(&h->defL, npix) == cudaSuccess;
+  h->Wg = guide_pitch(W, radius);
+  const size_t ngp = (size_t)guide_rows(H, radius) * h->Wg;
+  ok &= cudaMalloc(&h->gpadL, ngp * 4) == cudaSuccess;
+  ok &= cudaMalloc(&h->gpadR, ngp * 4) == cudaSuccess;
   ok &= cudaMalloc(&h->bitsL, (size_t)H * h->Wb * 4) == cudaSuccess;
   ok &= cudaMalloc(&h->bitsR, (size_t)H * h->Wb * 4) == cudaSuccess;
-  ok &= cudaMalloc(&h->defR, npix) == cudaSuccess;
   ok &= cudaMalloc(&h->volL, nvol * 4) == cudaSuccess;
   ok &= cudaMalloc(&h->volR, nvol * 4) == cudaSuccess;
   ok &= cudaMalloc(&h->dL, npix * 4) == cudaSuccess;
@@ -133,16 +139,11 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
   // margins (and never-written rows) of the volumes hold the undefined cost
   k_fill<<<1184, 256>>>(h->volL, nvol, kUndef);
   k_fill<<<1184, 256>>>(h->volR, nvol, kUndef);
+  k_fill<<<256, 256>>>(h->gpadL, ngp, kGuideUndef);  // margins: taps outside the frame
+  k_fill<<<256, 256>>>(h->gpadR, ngp, kGuideUndef);
   cudaMemset(h->tile_stats, 0, 3 * sizeof(unsigned long long));
-  {  // ω_r(|Δ|) at index Δ + 255 for Δ in [-255, 255]; zero tail for undefined taps
-    float lut[kLut];
-    for (int i = 0; i < kLut; ++i) lut[i] = (i - 255 >= -255 && i - 255 <= 255) ? h->wr[std::abs(i - 255)] : 0.f;
-    cudaMemcpy(h->lut, lut, sizeof(lut), cudaMemcpyHostToDevice);
-  }
   cudaMemset(h->dL, 0xff, npix * 4);
   cudaMemset(h->dR, 0xff, npix * 4);
-  cudaMemset(h->defL, 0, npix);
-  cudaMemset(h->defR, 0, npix);
   cudaMemset(h->bitsL, 0, (size_t)H * h->Wb * 4);
   cudaMemset(h->bitsR, 0, (size_t)H * h->Wb * 4);
   if (cuda_check(cudaDeviceSynchronize(), "fbs_create init") != FBS_OK) {
@@ -184,9 +185,9 @@ extern "C" void fbs_destroy(fbs_ctx* h) {
 static void fill_agg_args(const fbs_ctx* h, AggArgs& a) {
   a.W = h->W; a.H = h->H; a.D = h->D; a.d_min = h->d_min; a.d_max = h->d_max;
   a.nblk = h->nblk; a.Wv = h->Wv;
-  std::memcpy(a.wd, h->wd, sizeof(a.wd));
-  a.lut = reinterpret_cast<const float4*>(h->lut);
-  a.goffL = h->goffL; a.goffR = h->goffR;
+  std::memcpy(a.cd, h->cd, sizeof(a.cd));
+  a.nkr = h->nkr;
+  a.gpadL = h->gpadL; a.gpadR = h->gpadR; a.Wg = h->Wg;
 }
 
 // Launch with programmatic stream serialization (PDL): the kernel may begin
@@ -235,9 +236,9 @@ static int run_rows(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0, i
     CostArgs ca;
     ca.W = W; ca.H = H; ca.D = h->D; ca.d_min = h->d_min; ca.nblk = h->nblk; ca.Wv = h->Wv; ca.R = R;
     ca.r0 = c0; ca.r1 = c1;
-    ca.L = L; ca.Rimg = Rimg; ca.volL = h->volL; ca.volR = h->volR; ca.defL = h->defL; ca.defR = h->defR;
+    ca.L = L; ca.Rimg = Rimg; ca.volL = h->volL; ca.volR = h->volR;
     ca.bitsL = h->bitsL; ca.bitsR = h->bitsR; ca.Wb = h->Wb;
-    ca.goffL = h->goffL; ca.goffR = h->goffR;
+    ca.gpadL = h->gpadL; ca.gpadR = h->gpadR; ca.Wg = h->Wg;
     const int ocount = kCX + h->nblk * kDB - 1;
     const size_t smem = (size_t)(kCX + ocount) * (sizeof(uint4) + sizeof(float));
     dim3 grd((W + kCX - 1) / kCX, c1 - c0, 2);
@@ -248,7 +249,7 @@ static int run_rows(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0, i
   AggArgs a;
   fill_agg_args(h, a);
   a.r0 = r0; a.r1 = r1; a.ty0 = ty0;
-  a.volL = h->volL; a.volR = h->volR; a.L = L; a.Rimg = Rimg; a.defL = h->defL; a.defR = h->defR;
+  a.volL = h->volL; a.volR = h->volR;
   a.bitsL = h->bitsL; a.bitsR = h->bitsR; a.Wb = h->Wb;
   a.dL = h->dL; a.dR = h->dR; a.aggL = h->aggL; a.exportR = aggR_exp;
   a.tile_stats = ev ? h->tile_stats : nullptr;

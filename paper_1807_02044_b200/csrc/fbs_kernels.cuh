@@ -64,10 +64,15 @@ constexpr int kTYMax = kPYMax * 2;                // tallest CTA tile of any rad
 __host__ __device__ constexpr int agg_tile_h(int R) { return (R >= 6 ? 4 : kPYMax) * 2; }
 
 constexpr int kCX = 64;          // cost kernel: pixels per CTA (multiple of 32)
-// Range-weight LUT indexed by Δ + 255 for Δ = i(q) - i(p) in [-255, 255]; an
-// undefined tap q stores kGuideSent instead of i(q) + 255, landing in the zero tail.
-constexpr int kGuideSent = 1021;
-constexpr int kLut = 1024;
+// Padded guide images for k_agg (written by k_cost): i(q) as a float, with an
+// R-pixel margin of kGuideUndef outside the frame.  A pixel whose own block is
+// undefined stores i + kGuideFlag: as a tap q it is >= 2^23 - 255 away from any
+// intensity, so ω_r flushes to exactly +0 (for γ_r <= FBS_MAX_SIGMA_R), and as a
+// centre p its intensity is recovered exactly (i + 2^23 is exact in fp32).
+constexpr float kGuideUndef = 1e30f;
+constexpr float kGuideFlag = 8388608.0f;
+__host__ __device__ constexpr int guide_pitch(int W, int R) { return ((W + 15) / 16 * 16 + 2 * R + 4 + 3) / 4 * 4; }
+__host__ __device__ constexpr int guide_rows(int H, int R) { return (H + kTYMax - 1) / kTYMax * kTYMax + kTYMax + 2 * R; }
 
 // Cost volume layout: [Hv][nblk][Wv][64] floats; pixel (x, y), disparity index
 // di = b*64 + dl lives at ((vy*nblk + b)*Wv + vx)*64 + dl with vy = y + R,
@@ -82,9 +87,9 @@ struct CostArgs {
   int W, H, D, d_min, nblk, Wv, R, r0, r1, Wb;  // [r0, r1): cost rows; Wb = words per mask row
   const uint8_t *L, *Rimg;
   float *volL, *volR;
-  uint8_t *defL, *defR;                         // block-defined masks (bytes), rows [r0, r1)
-  uint32_t *bitsL, *bitsR;                      // the same masks bit-packed [H][Wb]
-  int32_t *goffL, *goffR;                       // k_agg guide tiles: 4*(i+255), or 4*kGuideSent if undefined
+  uint32_t *bitsL, *bitsR;                      // block-defined masks, bit-packed [H][Wb]
+  float *gpadL, *gpadR;                         // padded guide images [guide_rows][Wg] (k_agg)
+  int Wg;
 };
 
 // Eq.(2)(3) x 81 in integers: packed rows P (i(x-1) | i(x)<<8 | i(x+1)<<16 of rows
@@ -140,10 +145,8 @@ __device__ __forceinline__ void cost_side(const CostArgs& a, uint4* csm) {
       const bool ok = rs != 0.f;
       const unsigned bits = __ballot_sync(0xffffffffu, ok);  // kCX is a multiple of 32
       if (x0 + i < a.W) {
-        const size_t pi = (size_t)y * a.W + x0 + i;
-        const uint8_t* img = SIDE == 0 ? a.L : a.Rimg;
-        (SIDE == 0 ? a.defL : a.defR)[pi] = ok;
-        (SIDE == 0 ? a.goffL : a.goffR)[pi] = 4 * (ok ? (int)img[pi] + 255 : kGuideSent);
+        const float gi = (float)self_img[(size_t)y * a.W + x0 + i] + (ok ? 0.f : kGuideFlag);
+        (SIDE == 0 ? a.gpadL : a.gpadR)[(size_t)(y + a.R) * a.Wg + x0 + i + a.R] = gi;
       }
       if ((i & 31) == 0 && x0 + i < a.W) (SIDE == 0 ? a.bitsL : a.bitsR)[(size_t)y * a.Wb + (x0 + i) / 32] = bits;
     } else {
@@ -294,17 +297,16 @@ struct AggArgs {
   int W, H, D, d_min, d_max, nblk, Wv, r0, r1;  // output rows [r0, r1)
   int ty0;                       // first tile row (tiles anchored at multiples of the tile height)
   const float *volL, *volR;      // cost volumes (padded layout)
-  const uint8_t *L, *Rimg;       // guides (Eq.(8); right image guides the right volume, R#11)
-  const uint8_t *defL, *defR;    // block-defined masks
-  const uint32_t *bitsL, *bitsR; // the same masks bit-packed [H][Wb]
+  const float *gpadL, *gpadR;    // padded guide images (Eq.(8); the right image guides the right volume, R#11)
+  int Wg;
+  const uint32_t *bitsL, *bitsR; // block-defined masks, bit-packed [H][Wb]
   int Wb;
   int32_t *dL, *dR;              // WTA maps [H][W]
   float* aggL;                   // left aggregated costs, [H][nblk][W][64] (read by k_finalize)
   float* exportR;                // optional [H][W][D] right aggregated volume (debug)
   unsigned long long* tile_stats;  // optional [3]: FAST / EDGE / GENERAL (tile, d-block) counts
-  const int32_t *goffL, *goffR;  // guide tiles, written by k_cost
-  const float4* lut;             // ω_r(|Δ|) at Δ + 255 (Eq.(8)), zero tail, kLut floats (fbs_create)
-  float wd[(2 * kMaxRadius + 1) * (2 * kMaxRadius + 1)];  // ω_d, Eq.(7)
+  float cd[(2 * kMaxRadius + 1) * (2 * kMaxRadius + 1)];  // log2 ω_d = -log2(e)(dx²+dy²)/γ_d², Eq.(7)
+  float nkr;                                               // -log2(e)/γ_r²: log2 ω_r = nkr Δ², Eq.(8)
 };
 
 enum { kFast = 0, kEdge = 1, kGeneral = 2 };
@@ -324,41 +326,76 @@ struct AggSmem {
   static constexpr int K1 = 2 * R + 1;
   static constexpr int WPW = AggGeom<R>::PY * K1 * K1 * kPX;  // weights per warp
   static constexpr int NW = AggGeom<R>::NW;
-  static constexpr int GW = kTX + 2 * R, GH = AggGeom<R>::TY + 2 * R;
+  static constexpr int GW = (kTX + 2 * R + 3) / 4 * 4, GH = AggGeom<R>::TY + 2 * R;
   float w[NW][WPW];                                 // [warp][py][dy][dx][px]
   float rinv[NW][32];                               // 1 / Σ_q w'(p,q), 0 if none
   float cs[NW][32][K1 + 1];                         // EDGE: 1 / suffix (left) or prefix (right) column sums
-  float lut[kLut];                                  // ω_r(|Δ|) at Δ + 255, zero tail
-  int g[GH * GW];                                   // 4*(i(q)+255), or 4*kGuideSent if undefined
+  float g[GH * GW];                                 // guide tile (padded image values, see kGuideFlag)
+  uint32_t cwb[NW][2][64];                          // classification words: current / next d-block
 };
 
-// Classify this CTA tile for d-block b (FAST / EDGE / GENERAL), conservatively:
-// EDGE if the frame edge cuts taps off, GENERAL if the other image has an
-// undefined block anywhere in the shifted range.  One mask word per thread.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Denominator form of one warp sub-tile (origin sx, sy; 4 x PY pixels) for d-block
+// b, exact and conservative: EDGE if the frame edge cuts taps off, GENERAL if the
+// other image has an undefined block anywhere in the shifted range.  The range
+// spans at most 16 rows x 4 mask words, two per lane: cw_load fetches them into
+// shared memory (cp.async, one d-block ahead), cw_classify consumes them.
+// Sub-tiles are anchored at multiples of (4, PY) in frame coordinates, so the
+// form a pixel gets never depends on the row band being computed.
 template <int R>
-__device__ __forceinline__ int classify(const AggArgs& a, int side, int x0, int y0, int b) {
-  const int qy0 = max(y0 - R, 1), qy1 = min(y0 + AggGeom<R>::TY - 1 + R, a.H - 2);
-  const int qx0 = max(x0 - R, 1), qx1 = min(x0 + kTX - 1 + R, a.W - 2);
-  const int d_lo = a.d_min + b * kDB, d_hi = min(d_lo + kDB - 1, a.d_max);
-  const uint32_t* bits = side == 0 ? a.bitsR : a.bitsL;
-  int edge = 0, tex = 0;
-  if (qy0 <= qy1 && qx0 <= qx1) {
-    int lo, hi;
+struct CwRange {
+  int qy0, lo, hi, edge, nw, rows, w0;
+  __device__ __forceinline__ CwRange(const AggArgs& a, int side, int sx, int sy, int b) {
+    qy0 = max(sy - R, 1);
+    const int qy1 = min(sy + AggGeom<R>::PY - 1 + R, a.H - 2);
+    const int qx0 = max(sx - R, 1), qx1 = min(sx + kPX - 1 + R, a.W - 2);
+    const int d_lo = a.d_min + b * kDB, d_hi = min(d_lo + kDB - 1, a.d_max);
     if (side == 0) { lo = qx0 - d_hi; hi = qx1 - d_lo; edge = lo < 1; lo = max(lo, 1); }
     else { lo = qx0 + d_lo; hi = qx1 + d_hi; edge = hi > a.W - 2; hi = min(hi, a.W - 2); }
-    if (lo <= hi) {
-      const int w0 = lo >> 5, nw = (hi >> 5) - w0 + 1, rows = qy1 - qy0 + 1;
-      for (int i = threadIdx.x; i < nw * rows; i += AggGeom<R>::THREADS) {
-        const int yy = qy0 + i / nw, wi = w0 + i % nw;
-        uint32_t m = 0xffffffffu;
-        if (wi == w0) m &= 0xffffffffu << (lo & 31);
-        if (wi == (hi >> 5)) m &= 0xffffffffu >> (31 - (hi & 31));
-        tex |= (~__ldg(bits + (size_t)yy * a.Wb + wi) & m) != 0u;
-      }
+    rows = (qy0 <= qy1 && qx0 <= qx1 && lo <= hi) ? qy1 - qy0 + 1 : 0;
+    w0 = lo >> 5;
+    nw = rows ? (hi >> 5) - w0 + 1 : 0;
+  }
+};
+template <int R>
+__device__ __forceinline__ void cw_load(const AggArgs& a, int side, int sx, int sy, int b, int lane,
+                                        uint32_t* cwb) {
+  const CwRange<R> g(a, side, sx, sy, b);
+  const uint32_t* bits = side == 0 ? a.bitsR : a.bitsL;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int i = lane + 32 * k;
+    if (i < g.nw * g.rows) cp_async4(cwb + i, bits + (size_t)(g.qy0 + i / g.nw) * a.Wb + g.w0 + i % g.nw);
+  }
+}
+template <int R>
+__device__ __forceinline__ int cw_classify(const AggArgs& a, int side, int sx, int sy, int b, int lane,
+                                           const uint32_t* cwb) {
+  const CwRange<R> g(a, side, sx, sy, b);
+  bool tex = false;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int i = lane + 32 * k;
+    if (i < g.nw * g.rows) {
+      const int wi = g.w0 + i % g.nw;
+      uint32_t m = 0xffffffffu;
+      if (wi == g.w0) m &= 0xffffffffu << (g.lo & 31);
+      if (wi == (g.hi >> 5)) m &= 0xffffffffu >> (31 - (g.hi & 31));
+      tex |= (~cwb[i] & m) != 0u;
     }
   }
-  if (__syncthreads_or(tex)) return kGeneral;
-  return edge ? kEdge : kFast;
+  if (__any_sync(0xffffffffu, tex)) return kGeneral;
+  return g.edge ? kEdge : kFast;
 }
 
 // 1/x for x > 0: MUFU reciprocal + one Newton step (<= 1 ulp; no slow path)
@@ -520,16 +557,19 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
   const int x0 = blockIdx.x * kTX, y0 = (a.ty0 + blockIdx.y) * kTY;
   const int wx = (warp % kNWX) * kPX, wy = (warp / kNWX) * kPY;
   const int sx = x0 + wx, sy = y0 + wy;
-  const uint8_t* guide = side == 0 ? a.L : a.Rimg;
 
   pdl_trigger();
-  for (int i = threadIdx.x; i < kLut / 4; i += kThreads) reinterpret_cast<float4*>(sm.lut)[i] = __ldg(a.lut + i);
   pdl_wait();  // everything below reads k_cost's outputs
-  const int32_t* goff = side == 0 ? a.goffL : a.goffR;
-  for (int i = threadIdx.x; i < GH * GW; i += kThreads) {
-    const int qx = x0 - R + i % GW, qy = y0 - R + i / GW;
-    sm.g[i] = (qx >= 0 && qx < a.W && qy >= 0 && qy < a.H) ? __ldg(goff + (size_t)qy * a.W + qx)
-                                                             : 4 * kGuideSent;
+  {  // guide tile (padded rows y0.., columns x0..: 16-B aligned) and the first
+     // d-block's classification words, all in flight at once
+    const float* src = (side == 0 ? a.gpadL : a.gpadR) + (size_t)y0 * a.Wg + x0;
+    for (int c = threadIdx.x; c < GH * (GW / 4); c += kThreads) {
+      const int row = c / (GW / 4), q = c % (GW / 4);
+      cp_async16(&sm.g[row * GW + 4 * q], src + (size_t)row * a.Wg + 4 * q);
+    }
+    cw_load<R>(a, side, sx, sy, 0, lane, sm.cwb[warp][0]);
+    cp_async_commit();
+    cp_async_wait_all();
   }
   __syncthreads();
 
@@ -537,11 +577,11 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
   //      their sum, and the window's column sums (EDGE denominators) ----
   if (lane < kPX * kPY) {
     const int py = lane / kPX, px = lane % kPX;
-    // pixels outside the frame get some in-frame guide value: their outputs are discarded
-    const int x = min(sx + px, a.W - 1), y = min(sy + py, a.H - 1);
+    // pixels outside the frame read the margin (kGuideUndef): their outputs are discarded
     float* wsm = sm.w[warp];
-    const char* lutp = reinterpret_cast<const char*>(sm.lut) - 4 * (int)guide[(size_t)y * a.W + x];
-    const int* gq = sm.g + (wy + py) * GW + (wx + px);
+    const float* gq = sm.g + (wy + py) * GW + (wx + px);
+    const float gc = gq[R * GW + R];                     // i(p) (+ kGuideFlag if undefined)
+    const float gp = gc >= kGuideFlag ? __fsub_rn(gc, kGuideFlag) : gc;
     float wsum = 0.f;
     float col[K1];
 #pragma unroll
@@ -553,20 +593,20 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
 #pragma unroll
     for (int dy0 = 0; dy0 < K1; dy0 += CH) {
       constexpr int NB = CH * K1;
-      int gv[NB];
-      float wv[NB];
+      float gv[NB];
 #pragma unroll
       for (int t = 0; t < NB; ++t) {
         const int dy = dy0 + t / K1, dx = t % K1;
-        gv[t] = dy < K1 ? gq[dy * GW + dx] : 0;
+        gv[t] = dy < K1 ? gq[dy * GW + dx] : 0.f;
       }
-#pragma unroll
-      for (int t = 0; t < NB; ++t) wv[t] = *reinterpret_cast<const float*>(lutp + gv[t]);
 #pragma unroll
       for (int t = 0; t < NB; ++t) {
         const int dy = dy0 + t / K1, dx = t % K1;
         if (dy < K1) {
-          const float w = __fmul_rn(a.wd[dy * K1 + dx], wv[t]);
+          // ω_d ω_r = 2^(cd(dx,dy) + nkr Δ²): Δ² exact, one MUFU.EX2 per tap
+          const float dd = __fsub_rn(gv[t], gp);
+          float w;
+          asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(w) : "f"(__fmaf_rn(__fmul_rn(dd, dd), a.nkr, a.cd[dy * K1 + dx])));
           col[dx] = __fadd_rn(col[dx], w);
           wsm[((py * K1 + dy) * K1 + dx) * kPX + px] = w;
         }
@@ -608,8 +648,17 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
   for (int b = 0; b < a.nblk; ++b) {
     // volume row (sy + py0 - R + r) + R = sy + py0 + r; column (sx - R + j) + R = sx + j
     const float* vb = vol + vol_at(sy + py0, b, sx, a.nblk, a.Wv) + 4 * dq;
-    const int cls = classify<R>(a, side, x0, y0, b);
-    if (a.tile_stats && threadIdx.x == 0) atomicAdd(a.tile_stats + cls, 1ull);
+    if (b > 0) {  // this d-block's words (issued one d-block ahead)
+      cp_async_wait_all();
+      __syncwarp();
+    }
+    const int cls = cw_classify<R>(a, side, sx, sy, b, lane, sm.cwb[warp][b & 1]);
+    __syncwarp();
+    if (b + 1 < a.nblk) {
+      cw_load<R>(a, side, sx, sy, b + 1, lane, sm.cwb[warp][(b + 1) & 1]);
+      cp_async_commit();
+    }
+    if (a.tile_stats && lane == 0) atomicAdd(a.tile_stats + cls, 1ull);
     unsigned long long k[16];
 #pragma unroll
     for (int s2 = kPX * HPY; s2 < 16; ++s2) k[s2] = 0ull;
