@@ -157,6 +157,7 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
   FBS_SMEM_ATTR(0) FBS_SMEM_ATTR(1) FBS_SMEM_ATTR(2) FBS_SMEM_ATTR(3) FBS_SMEM_ATTR(4)
   FBS_SMEM_ATTR(5) FBS_SMEM_ATTR(6)
 #undef FBS_SMEM_ATTR
+  cudaFuncSetAttribute(k_cost, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cost_smem_bytes(h->nblk));
   if (cuda_check(cudaGetLastError(), "fbs_create smem attributes") != FBS_OK) {
     free_all(h);
     delete h;
@@ -239,8 +240,7 @@ static int run_rows(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0, i
     ca.L = L; ca.Rimg = Rimg; ca.volL = h->volL; ca.volR = h->volR;
     ca.bitsL = h->bitsL; ca.bitsR = h->bitsR; ca.Wb = h->Wb;
     ca.gpadL = h->gpadL; ca.gpadR = h->gpadR; ca.Wg = h->Wg;
-    const int ocount = kCX + h->nblk * kDB - 1;
-    const size_t smem = (size_t)(kCX + ocount) * (sizeof(uint4) + sizeof(float));
+    const size_t smem = cost_smem_bytes(h->nblk);
     dim3 grd((W + kCX - 1) / kCX, c1 - c0, 2);
     k_cost<<<grd, 256, smem, s>>>(ca);
     h->launches += 1;

@@ -92,98 +92,124 @@ struct CostArgs {
   int Wg;
 };
 
-// Eq.(2)(3) x 81 in integers: packed rows P (i(x-1) | i(x)<<8 | i(x+1)<<16 of rows
-// y-1, y, y+1), S = Σ i, and V^{-1/2} (0 when the block is a border or
-// textureless block, or x is outside the image: σ < σ_floor <=> V = 0, R#7).
-__device__ __forceinline__ void block_pack(const uint8_t* __restrict__ img, int W, int H, int x, int y,
-                                           uint4& P, float& rs) {
-  P = make_uint4(0u, 0u, 0u, 0u);
-  rs = 0.f;
-  if (x < 1 || x > W - 2 || y < 1 || y > H - 2) return;
-  int s = 0, q = 0;
-  uint32_t pk[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    const uint8_t* row = img + (size_t)(y - 1 + k) * W + x - 1;
-    const uint32_t a = row[0], b = row[1], c = row[2];
-    pk[k] = a | (b << 8) | (c << 16);
-    s += (int)(a + b + c);
-    q += (int)(a * a + b * b + c * c);
-  }
-  const int V = 9 * q - s * s;
-  P = make_uint4(pk[0], pk[1], pk[2], (uint32_t)s);
-  if (V > 0) {  // V^{-1/2}: MUFU rsqrt + one Newton step (~1 ulp, no slow-path branch)
-    const float v = (float)V;  // exact: V < 2^24
-    float r;
-    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
-    rs = __fmul_rn(r, __fmaf_rn(__fmul_rn(-0.5f * v, r), r, 1.5f));
-  }
-}
+// Cost kernel shared memory for a staging of ncol image columns and nblkpos
+// block positions (self + other image).
+//   column c of row y:  packed column P = i(x,y-1) | i(x,y) << 8 | i(x,y+1) << 16,
+//                        column sum and sum of squares (Eq.(2)(3) split by columns)
+//   block at x:          S = Σ_3x3 i, r = V^{-1/2} with V = 9 Σ i² - S² (exact
+//                        integers < 2^24), r = 0 for a border or textureless block
+//                        (σ < σ_floor <=> V = 0, R#7)
+struct CostStage {
+  uint32_t* cP;
+  int* cS;
+  int* cQ;
+  int2* bSR;  // (S, r bits)
+};
 
 // side 0: left volume c(x, x-d); side 1: right volume c(x'+d, x').  The same
 // function of the same operands ((N · r_left) · r_right), so
 // right(u-d,v,d) == left(u,v,d) bit-exactly.
 template <int SIDE>
-__device__ __forceinline__ void cost_side(const CostArgs& a, uint4* csm) {
+__device__ __forceinline__ void cost_side(const CostArgs& a, unsigned char* smraw) {
   const int y = a.r0 + blockIdx.y;
   const int x0 = blockIdx.x * kCX;
   const int dspan = a.nblk * kDB;
   const uint8_t* self_img = SIDE == 0 ? a.L : a.Rimg;
   const uint8_t* oth_img = SIDE == 0 ? a.Rimg : a.L;
+  // other-image block positions olo .. olo + ocount - 1 (x -+ d over the block range)
   const int olo = SIDE == 0 ? x0 - a.d_min - dspan + 1 : x0 + a.d_min;
   const int ocount = kCX + dspan - 1;
-  uint4* sP = csm;
-  uint4* oP = csm + kCX;
-  float* sR = reinterpret_cast<float*>(csm + kCX + ocount);
-  float* oR = sR + kCX;
-  for (int i = threadIdx.x; i < kCX + ocount; i += blockDim.x) {
-    uint4 P;
-    float rs;
-    if (i < kCX) {
-      block_pack(self_img, a.W, a.H, x0 + i, y, P, rs);
-      sP[i] = P; sR[i] = rs;
+  const int ncs = kCX + 2, nco = ocount + 2;  // columns: self x0-1 .., other olo-1 ..
+  uint32_t* cP = reinterpret_cast<uint32_t*>(smraw);
+  int* cS = reinterpret_cast<int*>(cP + ncs + nco);
+  int* cQ = cS + ncs + nco;
+  int2* bSR = reinterpret_cast<int2*>(cQ + ncs + nco + ((ncs + nco) & 1));  // self kCX, then other ocount
+  const bool row_ok = y >= 1 && y <= a.H - 2;
+  // 1. columns (coalesced byte loads of the three rows)
+  for (int i = threadIdx.x; i < ncs + nco; i += blockDim.x) {
+    const bool self = i < ncs;
+    const int x = self ? x0 - 1 + i : olo - 1 + (i - ncs);
+    const uint8_t* img = self ? self_img : oth_img;
+    uint32_t P = 0u;
+    int cs = 0, cq = 0;
+    if (row_ok && x >= 0 && x < a.W) {
+      const uint32_t u0 = img[(size_t)(y - 1) * a.W + x], u1 = img[(size_t)y * a.W + x],
+                     u2 = img[(size_t)(y + 1) * a.W + x];
+      P = u0 | (u1 << 8) | (u2 << 16);
+      cs = (int)(u0 + u1 + u2);
+      cq = (int)(u0 * u0 + u1 * u1 + u2 * u2);
+    }
+    cP[i] = P; cS[i] = cs; cQ[i] = cq;
+  }
+  __syncthreads();
+  // 2. block statistics; the self blocks also write the guide image and the masks
+  for (int j = threadIdx.x; j < kCX + ocount; j += blockDim.x) {
+    const bool self = j < kCX;
+    const int c = self ? j : ncs + (j - kCX);  // first of the block's three columns
+    const int x = self ? x0 + j : olo + (j - kCX);
+    const int S = cS[c] + cS[c + 1] + cS[c + 2];
+    const int V = 9 * (cQ[c] + cQ[c + 1] + cQ[c + 2]) - S * S;
+    float rs = 0.f;
+    if (row_ok && x >= 1 && x <= a.W - 2 && V > 0) {  // MUFU rsqrt + one Newton step (~1 ulp)
+      const float v = (float)V;                        // exact: V < 2^24
+      float r;
+      asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+      rs = __fmul_rn(r, __fmaf_rn(__fmul_rn(-0.5f * v, r), r, 1.5f));
+    }
+    bSR[j] = make_int2(S, __float_as_int(rs));
+    if (self) {
       const bool ok = rs != 0.f;
       const unsigned bits = __ballot_sync(0xffffffffu, ok);  // kCX is a multiple of 32
-      if (x0 + i < a.W) {
-        const float gi = (float)self_img[(size_t)y * a.W + x0 + i] + (ok ? 0.f : kGuideFlag);
-        (SIDE == 0 ? a.gpadL : a.gpadR)[(size_t)(y + a.R) * a.Wg + x0 + i + a.R] = gi;
+      if (x < a.W) {
+        const float gi = (float)self_img[(size_t)y * a.W + x] + (ok ? 0.f : kGuideFlag);
+        (SIDE == 0 ? a.gpadL : a.gpadR)[(size_t)(y + a.R) * a.Wg + x + a.R] = gi;
       }
-      if ((i & 31) == 0 && x0 + i < a.W) (SIDE == 0 ? a.bitsL : a.bitsR)[(size_t)y * a.Wb + (x0 + i) / 32] = bits;
-    } else {
-      const int j = i - kCX;
-      block_pack(oth_img, a.W, a.H, olo + j, y, P, rs);
-      oP[j] = P; oR[j] = rs;
+      if ((j & 31) == 0 && x < a.W) (SIDE == 0 ? a.bitsL : a.bitsR)[(size_t)y * a.Wb + x / 32] = bits;
     }
   }
   __syncthreads();
+  // 3. values: warp <-> 8 consecutive pixels, lane <-> disparity pair.  The 3x3 dot
+  // product is the sum of three column dots (one DP4A each); along the 8 pixels a
+  // column dot is shared by three blocks, so 10 DP4A give 8 dot products.
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float* vol = SIDE == 0 ? a.volL : a.volR;
-  // warp w: the 8 consecutive pixels x0 + 8w .. x0 + 8w + 7 (unrolled: the volume
-  // and staging addresses of the 8 are immediate offsets of one base)
   constexpr int PPW = kCX / 8;
   const int xw = warp * PPW;
+  const int npx = min(PPW, a.W - (x0 + xw));
+  if (npx <= 0) return;
   float* vp = vol + vol_at(y + a.R, 0, x0 + xw + a.R, a.nblk, a.Wv) + 2 * lane;
   const size_t bstride = (size_t)a.Wv * kDB;  // next d-block of the same pixel
+  const uint32_t* cPs = cP + xw;               // self column of block xw + m: cPs[m .. m+2]
+  const int2* sSR = bSR + xw;
+  const int2* oSR = bSR + kCX;
   for (int b = 0; b < a.nblk; ++b) {
     const int di0 = b * kDB + 2 * lane;
     const bool pad0 = di0 >= a.D, pad1 = di0 + 1 >= a.D;
-    // other-image staging index of pixel xw and disparity index di0: xw -+ (d_min + di0) - olo
-    const int j0 = SIDE == 0 ? xw + dspan - 1 - di0 : xw + di0;
+    // other-image block index of (pixel xw + m, disparity index di0 + k): jo + m -+ k
+    const int jo = SIDE == 0 ? xw + dspan - 1 - di0 : xw + di0;
+    const uint32_t* cPo = cP + ncs + jo;  // other column of (m, k=0): cPo[m], k=1: cPo[m -+ 1]
+    uint32_t po[PPW + 3];                 // other columns jo + m - 1 (SIDE 0) / jo + m (SIDE 1)
+#pragma unroll
+    for (int m = 0; m < PPW + 3; ++m) po[m] = cPo[SIDE == 0 ? m - 1 : m];
+    int cd0[PPW + 2], cd1[PPW + 2];       // column dots for k = 0, 1
+#pragma unroll
+    for (int m = 0; m < PPW + 2; ++m) {
+      const uint32_t ps = cPs[m];
+      cd0[m] = (int)__dp4a(ps, SIDE == 0 ? po[m + 1] : po[m], 0u);
+      cd1[m] = (int)__dp4a(ps, SIDE == 0 ? po[m] : po[m + 1], 0u);
+    }
 #pragma unroll
     for (int u = 0; u < PPW; ++u) {
-      if (x0 + xw + u >= a.W) break;
-      const uint4 ps = sP[xw + u];
-      const float rsf = sR[xw + u];
+      if (u >= npx) break;
+      const int2 ss = sSR[u];
+      const float rsf = __int_as_float(ss.y);
       float o[2];
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
-        const int jk = SIDE == 0 ? j0 + u - k : j0 + u + k;
-        const uint4 po = oP[jk];
-        const float rof = oR[jk];
-        unsigned dot = __dp4a(ps.x, po.x, 0u);
-        dot = __dp4a(ps.y, po.y, dot);
-        dot = __dp4a(ps.z, po.z, dot);
-        const int N = 9 * (int)dot - (int)ps.w * (int)po.w;
+        const int2 so = oSR[SIDE == 0 ? jo + u - k : jo + u + k];
+        const float rof = __int_as_float(so.y);
+        const int dot = k == 0 ? cd0[u] + cd0[u + 1] + cd0[u + 2] : cd1[u] + cd1[u + 1] + cd1[u + 2];
+        const int N = 9 * dot - ss.x * so.x;
         const float rl = SIDE == 0 ? rsf : rof, rr = SIDE == 0 ? rof : rsf;
         const float c = fminf(1.0f, fmaxf(-1.0f, __fmul_rn(__fmul_rn((float)N, rl), rr)));  // clamp (R#8)
         o[k] = (rsf != 0.f && rof != 0.f) ? c : kUndef;
@@ -195,9 +221,13 @@ __device__ __forceinline__ void cost_side(const CostArgs& a, uint4* csm) {
   }
 }
 
+__host__ __device__ constexpr size_t cost_smem_bytes(int nblk) {
+  return (size_t)(kCX + 2 + kCX + nblk * kDB + 1) * 12 + 8 + (size_t)(kCX + kCX + nblk * kDB - 1) * 8;
+}
+
 // grid: (ceil(W/kCX), r1-r0, 2 sides); block 256 = 8 warps; warp <-> pixel, lane <-> d pair.
 __global__ void __launch_bounds__(256) k_cost(CostArgs a) {
-  extern __shared__ uint4 csm[];
+  extern __shared__ __align__(16) unsigned char csm[];
   pdl_trigger();  // k_agg may be scheduled now; it waits for our results in pdl_wait()
   if (blockIdx.z == 0) cost_side<0>(a, csm);
   else cost_side<1>(a, csm);
