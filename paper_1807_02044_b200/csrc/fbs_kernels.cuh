@@ -38,16 +38,6 @@ namespace fbs {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-// k_agg re-synchronises its warps at every d-block (one CTA barrier): warps that
-// drift apart execute different parts of the unrolled FMA stream, which does
-// not fit the instruction cache (measured: MB2014 aggregation 14.3 -> 13.0 ms).
-#ifndef FBS_BLOCK_SYNC
-#define FBS_BLOCK_SYNC 1
-#endif
-#ifndef FBS_CTA_FORM
-#define FBS_CTA_FORM 0
-#endif
-
 constexpr float kSent = -2.0f;   // undefined aggregated cost / exported cost (R#7)
 constexpr float kUndef = -0.0f;  // undefined cost inside the volumes (never a defined NCC value)
 constexpr int kMaxRadius = 6;    // FBS_MAX_RADIUS
@@ -690,21 +680,12 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
     const float* vb = vol + vol_at(sy + py0, b, sx, a.nblk, a.Wv) + 4 * dq;
     if (b > 0) {  // this d-block's words (issued one d-block ahead)
       cp_async_wait_all();
-#if FBS_BLOCK_SYNC
+      // one CTA barrier per d-block keeps the warps in lockstep: warps that drift
+      // apart run different parts of the unrolled FMA stream, which is larger than
+      // the instruction cache (measured: MB2014 aggregation 14.3 -> 13.0 ms)
       __syncthreads();
-#else
-      __syncwarp();
-#endif
     }
-#if FBS_CTA_FORM
-    int cls = cw_classify<R>(a, side, sx, sy, b, lane, sm.cwb[warp][b & 1]);
-    {  // one form for the whole CTA tile (every form is exact): the warps stay on one code path
-      const int g = __syncthreads_or(cls == kGeneral), e = __syncthreads_or(cls == kEdge);
-      cls = g ? kGeneral : (e ? kEdge : kFast);
-    }
-#else
     const int cls = cw_classify<R>(a, side, sx, sy, b, lane, sm.cwb[warp][b & 1]);
-#endif
     __syncwarp();
     if (b + 1 < a.nblk) {
       cw_load<R>(a, side, sx, sy, b + 1, lane, sm.cwb[warp][(b + 1) & 1]);
