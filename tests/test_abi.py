@@ -72,6 +72,7 @@ def test_sass_uses_ffma2():
     ((10, 10, 0, 5, 1, 0.0, 1.0), -2),
     ((10, 10, 0, 5, 1, 1.0, float("nan")), -2),
     ((10, 10, 0, 5, 7, 1.0, 1.0), -4),
+    ((10, 10, 0, 5, 1, 1.0, 2.0e5), -4),  # sigma_r > FBS_MAX_SIGMA_R
 ])
 def test_create_rejects_bad_params(lib, args, code):
     h = lib.fbs_create(*args)
