@@ -133,6 +133,18 @@ int fbs_compute_host(fbs_ctx* h, const uint8_t* left, const uint8_t* right, floa
                      fbs_stream_t stream);
 
 /*
+ * fbs_compute_host_batch — fbs_compute_host over n frames stored back to back
+ * in HOST memory (left/right: n x [H][W] uint8, disp_out: n x [H][W] float;
+ * pinned for the copies to be asynchronous).  Pipelined: frame i+1's upload and
+ * frame i-1's download run on the copy engines (two internal streams, created
+ * on first use and owned by the handle) while frame i computes on `stream`.
+ * Results are identical to n calls of fbs_compute.  Blocking: returns after
+ * the last map is in disp_out.  FBS_E_ARG for NULL pointers or n < 1.
+ */
+int fbs_compute_host_batch(fbs_ctx* h, const uint8_t* left, const uint8_t* right, int n,
+                           float* disp_out, fbs_stream_t stream);
+
+/*
  * fbs_debug_volumes — test-only export of the intermediate volumes, each
  * device float [H][W][D] indexed ((v*W+u)*D + d-d_min), FBS_SENTINEL where
  * undefined:

@@ -25,7 +25,7 @@ FBS_MAX_RADIUS = 6
 
 # every symbol include/fbs.h declares
 EXPORTS = ("fbs_create", "fbs_destroy", "fbs_last_error", "fbs_compute", "fbs_compute_rows",
-           "fbs_compute_batch", "fbs_compute_host", "fbs_debug_volumes", "fbs_debug_select",
+           "fbs_compute_batch", "fbs_compute_host", "fbs_compute_host_batch", "fbs_debug_volumes", "fbs_debug_select",
            "fbs_debug_maps", "fbs_stats", "fbs_profile_enable", "fbs_profile_read", "fbs_tile_stats")
 FBS_NSTAGES = 3
 STAGES = ("cost", "agg", "finalize")
@@ -58,6 +58,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.fbs_compute_rows.argtypes = [P, P, P, I, I, P, P]
     lib.fbs_compute_batch.argtypes = [P, P, P, I, P, P]
     lib.fbs_compute_host.argtypes = [P, P, P, P, P]
+    lib.fbs_compute_host_batch.argtypes = [P, P, P, I, P, P]
     lib.fbs_debug_volumes.argtypes = [P, P, P, P, P, P, P, P]
     lib.fbs_debug_select.argtypes = [P, P, P, P, P, P, P]
     lib.fbs_debug_maps.argtypes = [P, P, P, P, P, P, P]
@@ -65,7 +66,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.fbs_profile_enable.argtypes = [P, I]
     lib.fbs_profile_read.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I)]
     lib.fbs_tile_stats.argtypes = [P] + [ctypes.POINTER(ctypes.c_longlong)] * 3
-    for name in ("fbs_compute", "fbs_compute_rows", "fbs_compute_batch", "fbs_compute_host",
+    for name in ("fbs_compute", "fbs_compute_rows", "fbs_compute_batch", "fbs_compute_host", "fbs_compute_host_batch",
                  "fbs_debug_volumes", "fbs_debug_select", "fbs_debug_maps", "fbs_stats",
                  "fbs_profile_enable", "fbs_profile_read", "fbs_tile_stats"):
         getattr(lib, name).restype = I
@@ -127,6 +128,12 @@ def fbs_compute_host(h, left, right, disp_out, stream=None) -> None:
     """Host (CPU, ideally pinned) uint8 inputs and float output; blocking."""
     _check(load_library().fbs_compute_host(h, _ptr(left), _ptr(right), _ptr(disp_out),
                                            _stream(stream)))
+
+
+def fbs_compute_host_batch(h, left, right, n: int, disp_out, stream=None) -> None:
+    """n host frames back to back (pinned for asynchronous copies); pipelined, blocking."""
+    _check(load_library().fbs_compute_host_batch(h, _ptr(left), _ptr(right), n, _ptr(disp_out),
+                                                 _stream(stream)))
 
 
 def fbs_debug_volumes(h, left, right, cost_l=None, cost_r=None, agg_l=None, agg_r=None,
@@ -233,6 +240,19 @@ class FBS:
         if out is None:
             out = torch.empty((self.H, self.W), dtype=torch.float32, pin_memory=True)
         fbs_compute_host(self.h, left, right, out, stream)
+        return out
+
+    def compute_host_batch(self, left, right, out=None, stream=None):
+        """left/right: host uint8 [n][H][W] (pinned); returns host float [n][H][W]."""
+        import torch
+        if left.is_cuda or right.is_cuda or tuple(left.shape[1:]) != (self.H, self.W) or left.shape != right.shape:
+            raise ValueError("compute_host_batch: expected host uint8 [n][H][W] pairs")
+        if left.dtype != torch.uint8 or not left.is_contiguous() or not right.is_contiguous():
+            raise ValueError("compute_host_batch: expected contiguous uint8 tensors")
+        n = left.shape[0]
+        if out is None:
+            out = torch.empty((n, self.H, self.W), dtype=torch.float32, pin_memory=True)
+        fbs_compute_host_batch(self.h, left, right, n, out, stream)
         return out
 
     def volumes(self, left, right, stream=None):

@@ -33,8 +33,10 @@ struct fbs_ctx {
   float *volL, *volR;
   int32_t *dL, *dR;
   float* aggL;       // left aggregated costs [H][nblk][W][64] (k_agg -> k_finalize)
-  uint8_t *hL, *hR;  // device staging for fbs_compute_host
+  uint8_t *hL, *hR;  // device staging for fbs_compute_host[_batch]: two frame slots each
   float* hOut;
+  cudaStream_t cs_in, cs_out;          // copy streams of the host path (created on first use)
+  cudaEvent_t ev_in[2], ev_done[2], ev_out[2];
   unsigned long long* tile_stats;  // device [3] FAST/EDGE/GENERAL, counting when prof_ev is set
   int launches;
   // live profiling (fbs_profile_enable): kEv events per frame
@@ -58,7 +60,21 @@ static int cuda_check(cudaError_t e, const char* what) {
 
 extern "C" const char* fbs_last_error(void) { return g_err.c_str(); }
 
+static void free_host_path(fbs_ctx* h) {
+  if (h->cs_in) {
+    cudaStreamDestroy(h->cs_in);
+    cudaStreamDestroy(h->cs_out);
+    for (int k = 0; k < 2; ++k) {
+      cudaEventDestroy(h->ev_in[k]);
+      cudaEventDestroy(h->ev_done[k]);
+      cudaEventDestroy(h->ev_out[k]);
+    }
+    h->cs_in = h->cs_out = nullptr;
+  }
+}
+
 static void free_all(fbs_ctx* h) {
+  free_host_path(h);
   void* ptrs[] = {h->gpadL, h->gpadR, h->bitsL, h->bitsR, h->volL, h->volR, h->dL, h->dR, h->aggL, h->hL, h->hR, h->hOut,
                   h->tile_stats};
   for (void* p : ptrs)
@@ -297,24 +313,58 @@ extern "C" int fbs_compute_batch(fbs_ctx* h, const uint8_t* left, const uint8_t*
   return FBS_OK;
 }
 
-extern "C" int fbs_compute_host(fbs_ctx* h, const uint8_t* left, const uint8_t* right, float* disp_out,
-                                fbs_stream_t stream) {
-  if (!h || !left || !right || !disp_out) return fail(FBS_E_ARG, "fbs_compute_host: NULL argument");
+// Host path: frame i's copies in (stream cs_in), compute (caller's stream) and
+// copy out (cs_out) are ordered by events; two staging slots let frame i+1's
+// upload and frame i-1's download run on the copy engines while frame i computes.
+extern "C" int fbs_compute_host_batch(fbs_ctx* h, const uint8_t* left, const uint8_t* right, int n,
+                                      float* disp_out, fbs_stream_t stream) {
+  if (!h || !left || !right || !disp_out) return fail(FBS_E_ARG, "fbs_compute_host_batch: NULL argument");
+  if (n < 1) return fail(FBS_E_ARG, "fbs_compute_host_batch: n must be >= 1");
   const size_t npix = (size_t)h->W * h->H;
   cudaStream_t s = (cudaStream_t)stream;
   if (!h->hL) {
-    if (cudaMalloc(&h->hL, npix) != cudaSuccess || cudaMalloc(&h->hR, npix) != cudaSuccess ||
-        cudaMalloc(&h->hOut, npix * 4) != cudaSuccess) {
+    bool ok = cudaMalloc(&h->hL, 2 * npix) == cudaSuccess && cudaMalloc(&h->hR, 2 * npix) == cudaSuccess &&
+              cudaMalloc(&h->hOut, 2 * npix * 4) == cudaSuccess;
+    ok = ok && cudaStreamCreateWithFlags(&h->cs_in, cudaStreamNonBlocking) == cudaSuccess &&
+         cudaStreamCreateWithFlags(&h->cs_out, cudaStreamNonBlocking) == cudaSuccess;
+    for (int k = 0; ok && k < 2; ++k)
+      ok = cudaEventCreateWithFlags(&h->ev_in[k], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&h->ev_done[k], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&h->ev_out[k], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {
       cudaGetLastError();
-      return fail(FBS_E_OOM, "fbs_compute_host: staging allocation failed");
+      return fail(FBS_E_OOM, "fbs_compute_host_batch: staging allocation failed");
     }
   }
   int rc;
-  if ((rc = cuda_check(cudaMemcpyAsync(h->hL, left, npix, cudaMemcpyHostToDevice, s), "H2D left"))) return rc;
-  if ((rc = cuda_check(cudaMemcpyAsync(h->hR, right, npix, cudaMemcpyHostToDevice, s), "H2D right"))) return rc;
-  if ((rc = fbs_compute(h, h->hL, h->hR, h->hOut, stream))) return rc;
-  if ((rc = cuda_check(cudaMemcpyAsync(disp_out, h->hOut, npix * 4, cudaMemcpyDeviceToHost, s), "D2H"))) return rc;
-  return cuda_check(cudaStreamSynchronize(s), "fbs_compute_host sync");
+  for (int i = 0; i < n; ++i) {
+    const int k = i & 1;
+    uint8_t *dl = h->hL + k * npix, *dr = h->hR + k * npix;
+    float* dout = h->hOut + k * npix;
+    if (i >= 2) cudaStreamWaitEvent(h->cs_in, h->ev_done[k], 0);  // slot k's inputs consumed (frame i-2)
+    if ((rc = cuda_check(cudaMemcpyAsync(dl, left + i * npix, npix, cudaMemcpyHostToDevice, h->cs_in), "H2D left")))
+      return rc;
+    if ((rc = cuda_check(cudaMemcpyAsync(dr, right + i * npix, npix, cudaMemcpyHostToDevice, h->cs_in), "H2D right")))
+      return rc;
+    cudaEventRecord(h->ev_in[k], h->cs_in);
+    cudaStreamWaitEvent(s, h->ev_in[k], 0);
+    if (i >= 2) cudaStreamWaitEvent(s, h->ev_out[k], 0);  // slot k's map downloaded (frame i-2)
+    if ((rc = fbs_compute(h, dl, dr, dout, stream))) return rc;
+    cudaEventRecord(h->ev_done[k], s);
+    cudaStreamWaitEvent(h->cs_out, h->ev_done[k], 0);
+    if ((rc = cuda_check(cudaMemcpyAsync(disp_out + i * npix, dout, npix * 4, cudaMemcpyDeviceToHost, h->cs_out),
+                         "D2H")))
+      return rc;
+    cudaEventRecord(h->ev_out[k], h->cs_out);
+  }
+  if ((rc = cuda_check(cudaStreamSynchronize(h->cs_out), "fbs_compute_host_batch sync"))) return rc;
+  return cuda_check(cudaStreamSynchronize(s), "fbs_compute_host_batch sync");
+}
+
+extern "C" int fbs_compute_host(fbs_ctx* h, const uint8_t* left, const uint8_t* right, float* disp_out,
+                                fbs_stream_t stream) {
+  if (!h || !left || !right || !disp_out) return fail(FBS_E_ARG, "fbs_compute_host: NULL argument");
+  return fbs_compute_host_batch(h, left, right, 1, disp_out, stream);
 }
 
 extern "C" int fbs_debug_volumes(fbs_ctx* h, const uint8_t* left, const uint8_t* right, float* cost_l,

@@ -162,6 +162,14 @@ def test_batch_host_and_determinism(fbs):
         hl = torch.from_numpy(L).pin_memory(); hr = torch.from_numpy(R).pin_memory()
         host = m.compute_host(hl, hr).numpy()
         assert np.array_equal(host.view(np.uint32), one.view(np.uint32))
+    # pipelined host batch (odd length: both staging slots, a ragged last pair)
+    for n in (1, 2, 5):
+        idx = [i % len(pairs) for i in range(n)]
+        hl = torch.from_numpy(np.stack([pairs[i][0] for i in idx])).pin_memory()
+        hr = torch.from_numpy(np.stack([pairs[i][1] for i in idx])).pin_memory()
+        hb = m.compute_host_batch(hl, hr).numpy()
+        for j, i in enumerate(idx):
+            assert np.array_equal(hb[j].view(np.uint32), batch[i].view(np.uint32)), (n, j)
 
 
 @pytest.mark.parametrize("cfgname,npts", [("kitti", 400), ("mb2014", 160)])
