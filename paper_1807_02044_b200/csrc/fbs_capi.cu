@@ -33,6 +33,7 @@ struct fbs_ctx {
   float *volL, *volR;
   int32_t *dL, *dR;
   float* aggL;       // left aggregated costs [H][nblk][W][64] (k_agg -> k_finalize)
+  float4* agg3;      // one d-block: (c(d*-1), c(d*), c(d*+1)) per left pixel [H][W] (k_agg -> k_finalize)
   uint8_t *hL, *hR;  // device staging for fbs_compute_host[_batch]: two frame slots each
   float* hOut;
   cudaStream_t cs_in, cs_out;          // copy streams of the host path (created on first use)
@@ -75,7 +76,7 @@ static void free_host_path(fbs_ctx* h) {
 
 static void free_all(fbs_ctx* h) {
   free_host_path(h);
-  void* ptrs[] = {h->gpadL, h->gpadR, h->bitsL, h->bitsR, h->volL, h->volR, h->dL, h->dR, h->aggL, h->hL, h->hR, h->hOut,
+  void* ptrs[] = {h->gpadL, h->gpadR, h->bitsL, h->bitsR, h->volL, h->volR, h->dL, h->dR, h->aggL, h->agg3, h->hL, h->hR, h->hOut,
                   h->tile_stats};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -144,6 +145,7 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
   ok &= cudaMalloc(&h->dL, npix * 4) == cudaSuccess;
   ok &= cudaMalloc(&h->dR, npix * 4) == cudaSuccess;
   ok &= cudaMalloc(&h->aggL, npix * h->nblk * kDB * sizeof(float)) == cudaSuccess;
+  ok &= cudaMalloc(&h->agg3, npix * sizeof(float4)) == cudaSuccess;
   ok &= cudaMalloc(&h->tile_stats, 3 * sizeof(unsigned long long)) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
@@ -268,6 +270,9 @@ static int run_rows(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0, i
   a.volL = h->volL; a.volR = h->volR;
   a.bitsL = h->bitsL; a.bitsR = h->bitsR; a.Wb = h->Wb;
   a.dL = h->dL; a.dR = h->dR; a.aggL = h->aggL; a.exportR = aggR_exp;
+  // one d-block: the left costs stay on chip and only Eq.(10)'s three are stored
+  // (unless the debug export wants the whole left volume)
+  a.agg3 = (h->nblk == 1 && !aggL_exp) ? h->agg3 : nullptr;
   a.tile_stats = ev ? h->tile_stats : nullptr;
   launch_agg(h, a, ty1, s);
   h->launches += 1;
@@ -275,7 +280,7 @@ static int run_rows(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0, i
   {
     dim3 grd((W + 127) / 128, r1 - r0);
     launch_pdl(k_finalize, grd, dim3(128), 0, s, (const int32_t*)h->dL, (const int32_t*)h->dR,
-               (const float*)h->aggL, h->nblk, W, r0, r1, h->d_min, h->d_max, out);
+               (const float*)h->aggL, (const float4*)a.agg3, h->nblk, W, r0, r1, h->d_min, h->d_max, out);
     h->launches += 1;
   }
   if (ev) cudaEventRecord(ev[3], s);
@@ -395,7 +400,8 @@ extern "C" int fbs_debug_select(fbs_ctx* h, const float* agg_l, const float* agg
   k_select_wta<<<nb, 256, 0, s>>>(agg_l, h->W, h->H, h->D, h->d_min, h->nblk, h->dL, h->aggL);
   if (disp_out) {
     dim3 grd((h->W + 127) / 128, h->H);
-    k_finalize<<<grd, 128, 0, s>>>(h->dL, h->dR, h->aggL, h->nblk, h->W, 0, h->H, h->d_min, h->d_max, disp_out);
+    k_finalize<<<grd, 128, 0, s>>>(h->dL, h->dR, h->aggL, nullptr, h->nblk, h->W, 0, h->H, h->d_min, h->d_max,
+                                   disp_out);
   }
   if (disp_l) cudaMemcpyAsync(disp_l, h->dL, npix * 4, cudaMemcpyDeviceToDevice, s);
   if (disp_r) cudaMemcpyAsync(disp_r, h->dR, npix * 4, cudaMemcpyDeviceToDevice, s);

@@ -274,8 +274,8 @@ __device__ __forceinline__ float finalize_pixel(int d_int, int e, float c0, floa
 // rows [r0, r1): out[(y - r0)*W + x]; aggregated costs from the left pass's
 // [H][nblk][W][64] store
 __global__ void k_finalize(const int32_t* __restrict__ dl, const int32_t* __restrict__ dr,
-                           const float* __restrict__ aggL, int nblk, int W, int r0, int r1, int d_min,
-                           int d_max, float* __restrict__ out) {
+                           const float* __restrict__ aggL, const float4* __restrict__ agg3, int nblk, int W,
+                           int r0, int r1, int d_min, int d_max, float* __restrict__ out) {
   pdl_wait();  // k_agg's maps
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = r0 + blockIdx.y;
@@ -285,7 +285,10 @@ __global__ void k_finalize(const int32_t* __restrict__ dl, const int32_t* __rest
   int e = -1;
   if (d >= 0 && x - d >= 0) e = dr[p - d];
   float c0 = kSent, cm = kSent, cp = kSent;
-  if (d >= 0) {
+  if (d >= 0 && agg3) {  // compact record written by k_agg
+    const float4 v = agg3[p];
+    cm = v.x; c0 = v.y; cp = v.z;
+  } else if (d >= 0) {
     auto at = [&](int di) { return aggL[(((size_t)y * nblk + di / kDB) * W + x) * kDB + di % kDB]; };
     const int di = d - d_min;
     c0 = at(di);
@@ -333,6 +336,8 @@ struct AggArgs {
   int Wb;
   int32_t *dL, *dR;              // WTA maps [H][W]
   float* aggL;                   // left aggregated costs, [H][nblk][W][64] (read by k_finalize)
+  float4* agg3;                  // if set (one d-block, no export): only (c(d*-1), c(d*), c(d*+1)) per
+                                 // left pixel, [H][W] float4, instead of aggL
   float* exportR;                // optional [H][W][D] right aggregated volume (debug)
   unsigned long long* tile_stats;  // optional [3]: FAST / EDGE / GENERAL (tile, d-block) counts
   float cd[(2 * kMaxRadius + 1) * (2 * kMaxRadius + 1)];  // log2 ω_d = -log2(e)(dx²+dy²)/γ_d², Eq.(7)
@@ -357,7 +362,12 @@ struct AggSmem {
   static constexpr int WPW = AggGeom<R>::PY * K1 * K1 * kPX;  // weights per warp
   static constexpr int NW = AggGeom<R>::NW;
   static constexpr int GW = (kTX + 2 * R + 3) / 4 * 4, GH = AggGeom<R>::TY + 2 * R;
+  // single-d-block frames keep the left pass's aggregated costs on chip: row py of
+  // the sub-tile ([px][64]) goes into its own weight row once that row is dead
+  // (room when K1² >= 64), else into a separate buffer
+  static constexpr bool kAlias = K1 * K1 >= kDB;
   float w[NW][WPW];                                 // [warp][py][dy][dx][px]
+  float val[NW][kAlias ? 4 : AggGeom<R>::PY * kPX * kDB];
   float rinv[NW][32];                               // 1 / Σ_q w'(p,q), 0 if none
   float cs[NW][32][K1 + 1];                         // EDGE: 1 / suffix (left) or prefix (right) column sums
   float g[GH * GW];                                 // guide tile (padded image values, see kGuideFlag)
@@ -674,6 +684,10 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
   const int half = lane >> 4, dq = lane & 15;       // half-warp, disparity quad within the block
   const int py0 = half * HPY;                       // first output row of this half in the sub-tile
   const float* wsm = sm.w[warp] + py0 * RS;
+  // on-chip aggregated costs of half-row pyl (compact mode): [px][64]
+  auto vrow = [&](int pyl) -> float* {
+    return AggSmem<R>::kAlias ? sm.w[warp] + (py0 + pyl) * RS : sm.val[warp] + (py0 + pyl) * kPX * kDB;
+  };
   unsigned long long best = 0ull;  // running best key of slot (lane & 15) of this half
   for (int b = 0; b < a.nblk; ++b) {
     // volume row (sy + py0 - R + r) + R = sy + py0 + r; column (sx - R + j) + R = sx + j
@@ -710,7 +724,9 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
       const int t = h ? 2 + h23 : h01;
       k[pyl * kPX + px] = ((unsigned long long)fkey(h ? b23 : b01) << 32) | (unsigned)(0xffff - (di0 + t));
       if (side == 0) {
-        if (x < a.W && y < a.H)
+        if (a.agg3)  // its weight row is dead: the stream of half-row pyl is done
+          *reinterpret_cast<float4*>(vrow(pyl) + px * kDB + 4 * dq) = agg;
+        else if (x < a.W && y < a.H)
           *reinterpret_cast<float4*>(a.aggL + (((size_t)y * a.nblk + b) * a.W + x) * kDB + 4 * dq) = agg;
       } else if (a.exportR && x < a.W && y >= a.r0 && y < a.r1) {
         float* er = a.exportR + ((size_t)y * a.W + x) * a.D;
@@ -723,6 +739,7 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
     if (cls != kGeneral) {
       float2 num[HPY][kPX][2];
       agg_num4<R, HPY>(vb, rowstride, wsm, num);
+      if (a.agg3) __syncwarp();  // every lane is done with the weights before they are overwritten
 #pragma unroll
       for (int pyl = 0; pyl < HPY; ++pyl)
 #pragma unroll
@@ -754,6 +771,7 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
       for (int pyl = 0; pyl < HPY; ++pyl) {
         float2 num[kPX][2], den[kPX][2];
         agg_num_den_row4<R>(vb + (size_t)pyl * rowstride, rowstride, wsm + pyl * RS, num, den);
+        if (a.agg3) __syncwarp();
 #pragma unroll
         for (int px = 0; px < kPX; ++px) {
           const float2 n0 = num[px][0], n1 = num[px][1], e0 = den[px][0], e1 = den[px][1];
@@ -768,6 +786,7 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
   }
 
   // ---- epilogue: lane l holds slot l & 15 of its half ----
+  if (a.agg3) __syncwarp();  // the half's on-chip costs are complete
   {
     const int s2 = lane & 15;
     if (s2 < kPX * HPY) {
@@ -776,6 +795,12 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
         const bool ok = (unsigned)(best >> 32) > fkey(kSent);
         const int d_int = ok ? a.d_min + (0xffff - (int)(best & 0xffffu)) : -1;
         (side == 0 ? a.dL : a.dR)[(size_t)y * a.W + x] = d_int;
+        if (side == 0 && a.agg3 && ok) {  // the three costs Eq.(10) needs
+          const float* vr = vrow(s2 / kPX) + (s2 % kPX) * kDB;
+          const int di = d_int - a.d_min;
+          a.agg3[(size_t)y * a.W + x] =
+              make_float4(di > 0 ? vr[di - 1] : kSent, vr[di], di + 1 < a.D ? vr[di + 1] : kSent, 0.f);
+        }
       }
     }
   }
