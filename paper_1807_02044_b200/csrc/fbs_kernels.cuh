@@ -362,6 +362,10 @@ struct AggSmem {
   static constexpr int WPW = AggGeom<R>::PY * K1 * K1 * kPX;  // weights per warp
   static constexpr int NW = AggGeom<R>::NW;
   static constexpr int GW = (kTX + 2 * R + 3) / 4 * 4, GH = AggGeom<R>::TY + 2 * R;
+  // shared-memory row stride of the guide tile: the prologue's 24 lanes read
+  // rows py (stride GWS) x columns px; a stride = 24 (mod 32) would put rows
+  // py and py + 4 in the same banks
+  static constexpr int GWS = GW % 32 == 24 ? GW + 4 : GW;
   // single-d-block frames keep the left pass's aggregated costs on chip: row py of
   // the sub-tile ([px][64]) goes into its own weight row once that row is dead
   // (room when K1² >= 64), else into a separate buffer
@@ -370,7 +374,7 @@ struct AggSmem {
   float val[NW][kAlias ? 4 : AggGeom<R>::PY * kPX * kDB];
   float rinv[NW][32];                               // 1 / Σ_q w'(p,q), 0 if none
   float cs[NW][32][K1 + 1];                         // EDGE: 1 / suffix (left) or prefix (right) column sums
-  float g[GH * GW];                                 // guide tile (padded image values, see kGuideFlag)
+  float g[GH * GWS];                                // guide tile (padded image values, see kGuideFlag)
   uint32_t cwb[NW][2][64];                          // classification words: current / next d-block
 };
 
@@ -388,7 +392,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // Denominator form of one warp sub-tile (origin sx, sy; 4 x PY pixels) for d-block
 // b, exact and conservative: EDGE if the frame edge cuts taps off, GENERAL if the
 // other image has an undefined block anywhere in the shifted range.  The range
-// spans at most 16 rows x 4 mask words, two per lane: cw_load fetches them into
+// spans at most 16 rows x 4 mask words (slot 4 row + word), two per lane: cw_load fetches them into
 // shared memory (cp.async, one d-block ahead), cw_classify consumes them.
 // Sub-tiles are anchored at multiples of (4, PY) in frame coordinates, so the
 // form a pixel gets never depends on the row band being computed.
@@ -413,9 +417,9 @@ __device__ __forceinline__ void cw_load(const AggArgs& a, int side, int sx, int 
   const CwRange<R> g(a, side, sx, sy, b);
   const uint32_t* bits = side == 0 ? a.bitsR : a.bitsL;
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const int i = lane + 32 * k;
-    if (i < g.nw * g.rows) cp_async4(cwb + i, bits + (size_t)(g.qy0 + i / g.nw) * a.Wb + g.w0 + i % g.nw);
+  for (int k = 0; k < 2; ++k) {  // slot i = 4 row + word (no division)
+    const int i = lane + 32 * k, row = i >> 2, wd = i & 3;
+    if (row < g.rows && wd < g.nw) cp_async4(cwb + i, bits + (size_t)(g.qy0 + row) * a.Wb + g.w0 + wd);
   }
 }
 template <int R>
@@ -425,9 +429,9 @@ __device__ __forceinline__ int cw_classify(const AggArgs& a, int side, int sx, i
   bool tex = false;
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
-    const int i = lane + 32 * k;
-    if (i < g.nw * g.rows) {
-      const int wi = g.w0 + i % g.nw;
+    const int i = lane + 32 * k, row = i >> 2, wd = i & 3;
+    if (row < g.rows && wd < g.nw) {
+      const int wi = g.w0 + wd;
       uint32_t m = 0xffffffffu;
       if (wi == g.w0) m &= 0xffffffffu << (g.lo & 31);
       if (wi == (g.hi >> 5)) m &= 0xffffffffu >> (31 - (g.hi & 31));
@@ -591,7 +595,7 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
   extern __shared__ __align__(16) unsigned char smraw[];
   AggSmem<R>& sm = *reinterpret_cast<AggSmem<R>*>(smraw);
   constexpr int K1 = 2 * R + 1;
-  constexpr int GW = AggSmem<R>::GW, GH = AggSmem<R>::GH;
+  constexpr int GW = AggSmem<R>::GW, GH = AggSmem<R>::GH, GWS = AggSmem<R>::GWS;
   const int side = blockIdx.z;  // 0: left volume / left guide, 1: right
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int x0 = blockIdx.x * kTX, y0 = (a.ty0 + blockIdx.y) * kTY;
@@ -605,7 +609,7 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
     const float* src = (side == 0 ? a.gpadL : a.gpadR) + (size_t)y0 * a.Wg + x0;
     for (int c = threadIdx.x; c < GH * (GW / 4); c += kThreads) {
       const int row = c / (GW / 4), q = c % (GW / 4);
-      cp_async16(&sm.g[row * GW + 4 * q], src + (size_t)row * a.Wg + 4 * q);
+      cp_async16(&sm.g[row * GWS + 4 * q], src + (size_t)row * a.Wg + 4 * q);
     }
     cw_load<R>(a, side, sx, sy, 0, lane, sm.cwb[warp][0]);
     cp_async_commit();
@@ -619,8 +623,8 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
     const int py = lane / kPX, px = lane % kPX;
     // pixels outside the frame read the margin (kGuideUndef): their outputs are discarded
     float* wsm = sm.w[warp];
-    const float* gq = sm.g + (wy + py) * GW + (wx + px);
-    const float gc = gq[R * GW + R];                     // i(p) (+ kGuideFlag if undefined)
+    const float* gq = sm.g + (wy + py) * GWS + (wx + px);
+    const float gc = gq[R * GWS + R];                     // i(p) (+ kGuideFlag if undefined)
     const float gp = gc >= kGuideFlag ? __fsub_rn(gc, kGuideFlag) : gc;
     float wsum = 0.f;
     float col[K1];
@@ -637,7 +641,7 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
 #pragma unroll
       for (int t = 0; t < NB; ++t) {
         const int dy = dy0 + t / K1, dx = t % K1;
-        gv[t] = dy < K1 ? gq[dy * GW + dx] : 0.f;
+        gv[t] = dy < K1 ? gq[dy * GWS + dx] : 0.f;
       }
 #pragma unroll
       for (int t = 0; t < NB; ++t) {
