@@ -719,9 +719,11 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
 #pragma unroll
     for (int t = 0; t < 4; ++t) pad[t] = di0 + t < a.D ? 0.f : -INFINITY;
     // aggregated costs (d = di0 .. di0+3) of half-row pixel (pyl, px) -> key, left store, export
-    auto emit = [&](int pyl, int px, float4 agg) {
+    // (FAST / EDGE pass the padded values themselves, PADDED = true)
+    auto emit = [&](int pyl, int px, float4 agg, bool padded) {
       const int y = sy + py0 + pyl, x = sx + px;
-      const float v0 = agg.x + pad[0], v1 = agg.y + pad[1], v2 = agg.z + pad[2], v3 = agg.w + pad[3];
+      const float v0 = padded ? agg.x : agg.x + pad[0], v1 = padded ? agg.y : agg.y + pad[1],
+                  v2 = padded ? agg.z : agg.z + pad[2], v3 = padded ? agg.w : agg.w + pad[3];
       const bool h01 = v1 > v0, h23 = v3 > v2;     // equal values keep the smaller d
       const float b01 = h01 ? v1 : v0, b23 = h23 ? v3 : v2;
       const bool h = b23 > b01;
@@ -765,10 +767,13 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
             }
           }
           const float2 n0 = num[pyl][px][0], n1 = num[pyl][px][1];
-          emit(pyl, px, make_float4(ri[0] > 0.f ? __fmul_rn(n0.x, ri[0]) : kSent,
-                                    ri[1] > 0.f ? __fmul_rn(n0.y, ri[1]) : kSent,
-                                    ri[2] > 0.f ? __fmul_rn(n1.x, ri[2]) : kSent,
-                                    ri[3] > 0.f ? __fmul_rn(n1.y, ri[3]) : kSent));
+          // num / den = num * (1/den) + 0, the padding (-inf) or, without any
+          // defined tap (1/den stored as 0), the sentinel folded into the addend
+          float off[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) off[t] = ri[t] > 0.f ? pad[t] : kSent;
+          emit(pyl, px, make_float4(__fmaf_rn(n0.x, ri[0], off[0]), __fmaf_rn(n0.y, ri[1], off[1]),
+                                    __fmaf_rn(n1.x, ri[2], off[2]), __fmaf_rn(n1.y, ri[3], off[3])), true);
         }
     } else {
 #pragma unroll
@@ -782,7 +787,7 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
           emit(pyl, px, make_float4(e0.x > 0.f ? __fmul_rn(n0.x, rcp_nr(e0.x)) : kSent,
                                     e0.y > 0.f ? __fmul_rn(n0.y, rcp_nr(e0.y)) : kSent,
                                     e1.x > 0.f ? __fmul_rn(n1.x, rcp_nr(e1.x)) : kSent,
-                                    e1.y > 0.f ? __fmul_rn(n1.y, rcp_nr(e1.y)) : kSent));
+                                    e1.y > 0.f ? __fmul_rn(n1.y, rcp_nr(e1.y)) : kSent), false);
         }
       }
     }
