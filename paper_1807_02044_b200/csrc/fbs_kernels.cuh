@@ -107,8 +107,8 @@ struct CostStage {
 };
 
 // side 0: left volume c(x, x-d); side 1: right volume c(x'+d, x').  The same
-// function of the same operands ((N · r_left) · r_right), so
-// right(u-d,v,d) == left(u,v,d) bit-exactly.
+// function of the same operands (N · (r_self · r_other), a commutative product),
+// so right(u-d,v,d) == left(u,v,d) bit-exactly.
 template <int SIDE>
 __device__ __forceinline__ void cost_side(const CostArgs& a, unsigned char* smraw) {
   const int y = a.r0 + blockIdx.y;
@@ -210,9 +210,11 @@ __device__ __forceinline__ void cost_side(const CostArgs& a, unsigned char* smra
         const float rof = __int_as_float(so.y);
         const int dot = k == 0 ? cd0[u] + cd0[u + 1] + cd0[u + 2] : cd1[u] + cd1[u + 1] + cd1[u + 2];
         const int N = 9 * dot - ss.x * so.x;
-        const float rl = SIDE == 0 ? rsf : rof, rr = SIDE == 0 ? rof : rsf;
-        const float c = fminf(1.0f, fmaxf(-1.0f, __fmul_rn(__fmul_rn((float)N, rl), rr)));  // clamp (R#8)
-        o[k] = (rsf != 0.f && rof != 0.f) ? c : kUndef;
+        // (V_l V_r)^{-1/2} as one product (commutative, so both sides get the same
+        // bits); zero iff either block is undefined (each factor >= 8.8e-4)
+        const float P = __fmul_rn(rsf, rof);
+        const float c = fminf(1.0f, fmaxf(-1.0f, __fmul_rn((float)N, P)));  // clamp (R#8)
+        o[k] = P != 0.f ? c : kUndef;
       }
       if (pad0) o[0] = kUndef;  // padded disparity slots of the last block
       if (pad1) o[1] = kUndef;
