@@ -76,7 +76,9 @@ typedef struct CUstream_st* fbs_stream_t;
  *   sigma_r       γ_r of Eq.(8), used verbatim as exp(-Δ^2/γ_r^2)   (> 0, finite,
  *                 <= FBS_MAX_SIGMA_R; larger values return FBS_E_UNSUPPORTED)
  * The NCC block half-width ϱ is fixed at 1 and the LRC tolerance at
- * 1 pixel (R#17).  Returns NULL on error (reason: fbs_last_error()).
+ * 1 pixel (R#17).  Environment: FBS_EMPTY_FORM=1 selects the
+ * aggregation variant that skips units whose costs are all undefined (large
+ * textureless regions; identical results, ~3 % slower on textured scenes).  Returns NULL on error (reason: fbs_last_error()).
  * Synchronises the device once (scratch initialisation); not graph-capturable.
  */
 fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, float sigma_s, float sigma_r);
@@ -199,7 +201,7 @@ int fbs_profile_enable(fbs_ctx* h, int n);
 int fbs_profile_read(fbs_ctx* h, double* stage_ms, int* ncalls);
 
 /*
- * fbs_tile_stats — how many (CTA tile, disparity block) units of the
+ * fbs_tile_stats — how many (warp sub-tile, disparity block) units of the
  * aggregation took each exact form of the Eq.(6) denominator during the
  * frames profiled since the last call (counting is on while
  * fbs_profile_enable is active):
@@ -208,9 +210,12 @@ int fbs_profile_read(fbs_ctx* h, double* stage_ms, int* ncalls);
  *   edge     the frame edge cuts taps off (left pass: x-d < 1; right pass:
  *            x+d > W-2): per-pixel prefix/suffix sums of column sums
  *   general  textureless blocks of the other image in range: explicit sum
+ *   empty    no block of the other image in range is defined: every cost the
+ *            unit reads is undefined, the aggregated costs are all SENTINEL
+ *            (no arithmetic)
  * Synchronises the device; resets the counts.  Any pointer may be NULL.
  */
-int fbs_tile_stats(fbs_ctx* h, long long* fast, long long* edge, long long* general);
+int fbs_tile_stats(fbs_ctx* h, long long* fast, long long* edge, long long* general, long long* empty);
 
 #ifdef __cplusplus
 }

@@ -65,7 +65,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.fbs_stats.argtypes = [P, ctypes.POINTER(I)]
     lib.fbs_profile_enable.argtypes = [P, I]
     lib.fbs_profile_read.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I)]
-    lib.fbs_tile_stats.argtypes = [P] + [ctypes.POINTER(ctypes.c_longlong)] * 3
+    lib.fbs_tile_stats.argtypes = [P] + [ctypes.POINTER(ctypes.c_longlong)] * 4
     for name in ("fbs_compute", "fbs_compute_rows", "fbs_compute_batch", "fbs_compute_host", "fbs_compute_host_batch",
                  "fbs_debug_volumes", "fbs_debug_select", "fbs_debug_maps", "fbs_stats",
                  "fbs_profile_enable", "fbs_profile_read", "fbs_tile_stats"):
@@ -171,10 +171,10 @@ def fbs_profile_read(h) -> tuple[dict, int]:
 
 
 def fbs_tile_stats(h) -> dict:
-    """(CTA tile, d-block) counts per denominator form since the last call."""
-    v = [ctypes.c_longlong(0) for _ in range(3)]
+    """(warp sub-tile, d-block) counts per denominator form since the last call."""
+    v = [ctypes.c_longlong(0) for _ in range(4)]
     _check(load_library().fbs_tile_stats(h, *(ctypes.byref(x) for x in v)))
-    return dict(zip(("fast", "edge", "general"), (x.value for x in v)))
+    return dict(zip(("fast", "edge", "general", "empty"), (x.value for x in v)))
 
 
 # ---------------------------------------------------------------------------

@@ -8,6 +8,7 @@
 //   k_finalize  LRC + subpixel -> disp_out                         Eq.(9)(10)
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -29,6 +30,7 @@ struct fbs_ctx {
   uint32_t *bitsL, *bitsR;
   float *gpadL, *gpadR;    // padded guide images for k_agg (k_cost), [guide_rows][Wg]
   int Wg;
+  bool empty_form;         // k_agg<R, true>: GENERAL units test for EMPTY (FBS_EMPTY_FORM=1 at create)
   int Wb;
   float *volL, *volR;
   int32_t *dL, *dR;
@@ -38,7 +40,7 @@ struct fbs_ctx {
   float* hOut;
   cudaStream_t cs_in, cs_out;          // copy streams of the host path (created on first use)
   cudaEvent_t ev_in[2], ev_done[2], ev_out[2];
-  unsigned long long* tile_stats;  // device [3] FAST/EDGE/GENERAL, counting when prof_ev is set
+  unsigned long long* tile_stats;  // device [4] FAST/EDGE/GENERAL/EMPTY, counting when prof_ev is set
   int launches;
   // live profiling (fbs_profile_enable): kEv events per frame
   cudaEvent_t* prof_ev;
@@ -118,6 +120,10 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
   h->Wv = (W + kTX - 1) / kTX * kTX + 2 * radius;
   h->Hv = (H + kTYMax - 1) / kTYMax * kTYMax + kTYMax + 2 * radius;
   h->sigma_s = sigma_s; h->sigma_r = sigma_r;
+  {  // tuning knob for scenes with large textureless regions
+    const char* e = std::getenv("FBS_EMPTY_FORM");
+    h->empty_form = e && e[0] == '1';
+  }
   cudaGetDevice(&h->device);
   // Eq.(7): ω_d(dx,dy) = exp(-(dx²+dy²)/γ_d²); Eq.(8): ω_r(Δ) = exp(-Δ²/γ_r²)  (R#10).
   // k_agg evaluates the product as one power of two: ω_d ω_r = 2^(cd(dx,dy) + nkr Δ²),
@@ -146,7 +152,7 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
   ok &= cudaMalloc(&h->dR, npix * 4) == cudaSuccess;
   ok &= cudaMalloc(&h->aggL, npix * h->nblk * kDB * sizeof(float)) == cudaSuccess;
   ok &= cudaMalloc(&h->agg3, npix * sizeof(float4)) == cudaSuccess;
-  ok &= cudaMalloc(&h->tile_stats, 3 * sizeof(unsigned long long)) == cudaSuccess;
+  ok &= cudaMalloc(&h->tile_stats, 4 * sizeof(unsigned long long)) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
     free_all(h);
@@ -159,7 +165,7 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
   k_fill<<<1184, 256>>>(h->volR, nvol, kUndef);
   k_fill<<<256, 256>>>(h->gpadL, ngp, kGuideUndef);  // margins: taps outside the frame
   k_fill<<<256, 256>>>(h->gpadR, ngp, kGuideUndef);
-  cudaMemset(h->tile_stats, 0, 3 * sizeof(unsigned long long));
+  cudaMemset(h->tile_stats, 0, 4 * sizeof(unsigned long long));
   cudaMemset(h->dL, 0xff, npix * 4);
   cudaMemset(h->dR, 0xff, npix * 4);
   cudaMemset(h->bitsL, 0, (size_t)H * h->Wb * 4);
@@ -171,7 +177,8 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
   }
   // opt-in shared memory for every aggregation variant
 #define FBS_SMEM_ATTR(RR) \
-  cudaFuncSetAttribute(k_agg<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(AggSmem<RR>));
+  cudaFuncSetAttribute(k_agg<RR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(AggSmem<RR>)); \
+  cudaFuncSetAttribute(k_agg<RR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(AggSmem<RR>));
   FBS_SMEM_ATTR(0) FBS_SMEM_ATTR(1) FBS_SMEM_ATTR(2) FBS_SMEM_ATTR(3) FBS_SMEM_ATTR(4)
   FBS_SMEM_ATTR(5) FBS_SMEM_ATTR(6)
 #undef FBS_SMEM_ATTR
@@ -231,7 +238,12 @@ static void launch_agg(const fbs_ctx* h, const AggArgs& a, int ty1, cudaStream_t
   dim3 grid((h->W + kTX - 1) / kTX, ty1 - a.ty0, 2);
   switch (h->R) {
 #define FBS_CASE(RR) \
-  case RR: launch_pdl(k_agg<RR>, grid, dim3(AggGeom<RR>::THREADS), sizeof(AggSmem<RR>), s, a); break;
+  case RR:                                                                                        \
+    if (h->empty_form)                                                                            \
+      launch_pdl(k_agg<RR, true>, grid, dim3(AggGeom<RR>::THREADS), sizeof(AggSmem<RR>), s, a);   \
+    else                                                                                          \
+      launch_pdl(k_agg<RR, false>, grid, dim3(AggGeom<RR>::THREADS), sizeof(AggSmem<RR>), s, a);  \
+    break;
     FBS_CASE(0) FBS_CASE(1) FBS_CASE(2) FBS_CASE(3) FBS_CASE(4) FBS_CASE(5) FBS_CASE(6)
 #undef FBS_CASE
   }
@@ -268,6 +280,7 @@ static int run_rows(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0, i
   fill_agg_args(h, a);
   a.r0 = r0; a.r1 = r1; a.ty0 = ty0;
   a.volL = h->volL; a.volR = h->volR;
+
   a.bitsL = h->bitsL; a.bitsR = h->bitsR; a.Wb = h->Wb;
   a.dL = h->dL; a.dR = h->dR; a.aggL = h->aggL; a.exportR = aggR_exp;
   // one d-block: the left costs stay on chip and only Eq.(10)'s three are stored
@@ -461,14 +474,16 @@ extern "C" int fbs_profile_read(fbs_ctx* h, double* stage_ms, int* ncalls) {
   return FBS_OK;
 }
 
-extern "C" int fbs_tile_stats(fbs_ctx* h, long long* fast, long long* edge, long long* general) {
+extern "C" int fbs_tile_stats(fbs_ctx* h, long long* fast, long long* edge, long long* general,
+                              long long* empty) {
   if (!h) return fail(FBS_E_ARG, "fbs_tile_stats: NULL handle");
-  unsigned long long v[3] = {0, 0, 0};
+  unsigned long long v[4] = {0, 0, 0, 0};
   int rc = cuda_check(cudaMemcpy(v, h->tile_stats, sizeof(v), cudaMemcpyDeviceToHost), "fbs_tile_stats");
   if (rc != FBS_OK) return rc;
   cudaMemset(h->tile_stats, 0, sizeof(v));
   if (fast) *fast = (long long)v[0];
   if (edge) *edge = (long long)v[1];
   if (general) *general = (long long)v[2];
+  if (empty) *empty = (long long)v[3];
   return FBS_OK;
 }

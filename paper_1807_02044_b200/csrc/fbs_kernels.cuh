@@ -341,12 +341,13 @@ struct AggArgs {
   float4* agg3;                  // if set (one d-block, no export): only (c(d*-1), c(d*), c(d*+1)) per
                                  // left pixel, [H][W] float4, instead of aggL
   float* exportR;                // optional [H][W][D] right aggregated volume (debug)
-  unsigned long long* tile_stats;  // optional [3]: FAST / EDGE / GENERAL (tile, d-block) counts
+  unsigned long long* tile_stats;  // optional [4]: FAST / EDGE / GENERAL / EMPTY (sub-tile, d-block) counts
   float cd[(2 * kMaxRadius + 1) * (2 * kMaxRadius + 1)];  // log2 ω_d = -log2(e)(dx²+dy²)/γ_d², Eq.(7)
   float nkr;                                               // -log2(e)/γ_r²: log2 ω_r = nkr Δ², Eq.(8)
 };
 
-enum { kFast = 0, kEdge = 1, kGeneral = 2 };
+enum { kFast = 0, kEdge = 1, kGeneral = 2, kEmpty = 3 };
+
 
 __device__ __forceinline__ void ffma2(float2& acc, float w, float2 c) {
   unsigned long long A, B = *reinterpret_cast<unsigned long long*>(&c);
@@ -442,6 +443,30 @@ __device__ __forceinline__ int cw_classify(const AggArgs& a, int side, int sx, i
   }
   if (__any_sync(0xffffffffu, tex)) return kGeneral;
   return g.edge ? kEdge : kFast;
+}
+
+// EMPTY (a special case of GENERAL, tested only there): no block of the other
+// image in range is defined, so every cost any window of the sub-tile reads at
+// this d-block is undefined and every aggregated cost is SENT, exactly.  (Kept
+// out of cw_classify: folding it in changed the code generated for the FAST
+// stream and cost 5 % at Teddy.)
+template <int R>
+__device__ __forceinline__ bool cw_empty(const AggArgs& a, int side, int sx, int sy, int b, int lane,
+                                         const uint32_t* cwb) {
+  const CwRange<R> g(a, side, sx, sy, b);
+  bool def = false;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int i = lane + 32 * k, row = i >> 2, wd = i & 3;
+    if (row < g.rows && wd < g.nw) {
+      const int wi = g.w0 + wd;
+      uint32_t m = 0xffffffffu;
+      if (wi == g.w0) m &= 0xffffffffu << (g.lo & 31);
+      if (wi == (g.hi >> 5)) m &= 0xffffffffu >> (31 - (g.hi & 31));
+      def |= (cwb[i] & m) != 0u;
+    }
+  }
+  return g.rows > 0 && !__any_sync(0xffffffffu, def);
 }
 
 // 1/x for x > 0: MUFU reciprocal + one Newton step (<= 1 ulp; no slow path)
@@ -588,8 +613,13 @@ __device__ __forceinline__ unsigned long long wta_butterfly16(unsigned long long
   return k[0];
 }
 
-// grid: (ceil(W/kTX), tile rows, 2 sides); block AggGeom<R>::THREADS (warps of 4 x PY sub-tiles)
-template <int R>
+// grid: (ceil(W/kTX), tile rows, 2 sides); block AggGeom<R>::THREADS (warps of 4 x PY sub-tiles).
+// EMPTY: whether GENERAL units test for the EMPTY special case (fbs_create reads
+// FBS_EMPTY_FORM).  A separate instantiation because the test perturbs the
+// code generated for the FAST stream: measured 3.5 % slower at Teddy, 19 %
+// faster on KITTI-shaped streams with textureless frames (an in-kernel switch
+// between both bodies compiled 20 % slower still).  Bit-identical results.
+template <int R, bool EMPTY>
 __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(const AggArgs a) {
   constexpr int kPY = AggGeom<R>::PY;
   constexpr int kTY = AggGeom<R>::TY;
@@ -606,6 +636,7 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
 
   pdl_trigger();
   pdl_wait();  // everything below reads k_cost's outputs
+
   {  // guide tile (padded rows y0.., columns x0..: 16-B aligned) and the first
      // d-block's classification words, all in flight at once
     const float* src = (side == 0 ? a.gpadL : a.gpadR) + (size_t)y0 * a.Wg + x0;
@@ -711,7 +742,7 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
       cw_load<R>(a, side, sx, sy, b + 1, lane, sm.cwb[warp][(b + 1) & 1]);
       cp_async_commit();
     }
-    if (a.tile_stats && lane == 0) atomicAdd(a.tile_stats + cls, 1ull);
+    if (a.tile_stats && lane == 0 && cls != kGeneral) atomicAdd(a.tile_stats + cls, 1ull);  // [4]: FAST EDGE GENERAL EMPTY
     unsigned long long k[16];
 #pragma unroll
     for (int s2 = kPX * HPY; s2 < 16; ++s2) k[s2] = 0ull;
@@ -777,7 +808,33 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
           emit(pyl, px, make_float4(__fmaf_rn(n0.x, ri[0], off[0]), __fmaf_rn(n0.y, ri[1], off[1]),
                                     __fmaf_rn(n1.x, ri[2], off[2]), __fmaf_rn(n1.y, ri[3], off[3])), true);
         }
+    } else if (EMPTY && cw_empty<R>(a, side, sx, sy, b, lane, sm.cwb[warp][b & 1])) {
+      if (a.tile_stats && lane == 0) atomicAdd(a.tile_stats + kEmpty, 1ull);
+      // every aggregated cost of the unit is SENT, which never wins the WTA (an
+      // all-SENT pixel stays INVALID whatever key it keeps): only the full left
+      // store and the debug export need the values
+      if (side == 0 && !a.agg3) {
+#pragma unroll 1
+        for (int s2 = 0; s2 < kPX * HPY; ++s2) {
+          const int y = sy + py0 + s2 / kPX, x = sx + s2 % kPX;
+          if (x < a.W && y < a.H)
+            *reinterpret_cast<float4*>(a.aggL + (((size_t)y * a.nblk + b) * a.W + x) * kDB + 4 * dq) =
+                make_float4(kSent, kSent, kSent, kSent);
+        }
+      } else if (side == 1 && a.exportR) {
+#pragma unroll 1
+        for (int s2 = 0; s2 < kPX * HPY; ++s2) {
+          const int y = sy + py0 + s2 / kPX, x = sx + s2 % kPX;
+          if (x < a.W && y >= a.r0 && y < a.r1)
+            for (int tt = 0; tt < 4; ++tt)
+              if (di0 + tt < a.D) a.exportR[((size_t)y * a.W + x) * a.D + di0 + tt] = kSent;
+        }
+      }
+      // no keys: zero keys leave the running best unchanged
+#pragma unroll
+      for (int s2 = 0; s2 < kPX * HPY; ++s2) k[s2] = 0ull;
     } else {
+      if (a.tile_stats && lane == 0) atomicAdd(a.tile_stats + kGeneral, 1ull);
 #pragma unroll
       for (int pyl = 0; pyl < HPY; ++pyl) {
         float2 num[kPX][2], den[kPX][2];

@@ -34,12 +34,16 @@ CASES = [
     ("three-dblocks", 150, 40, 0, 129, 2, "layered", 12, 3.0, 40.0),
     ("tsukuba", 384, 288, 0, 15, 4, "layered", 0x1808, 5.0, 32.0),
     ("teddy", 450, 375, 0, 59, 4, "layered", 0x1809, 5.0, 32.0),
+    # mostly textureless (70-94 % undefined blocks): EMPTY, GENERAL and EDGE units mixed
+    ("textureless", 160, 120, 0, 79, 4, "flat", 20, 5.0, 32.0),
 ]
 
 
 def make_pair(kind, W, H, d_min, d_max, seed):
     if kind == "layered":
         L, R, _, _ = synth.layered(W, H, d_min, d_max, seed, p_flat=0.3)
+    elif kind == "flat":
+        L, R, _, _ = synth.layered(W, H, d_min, d_max, seed, p_flat=0.9)
     elif kind.startswith("dot"):
         L, R = synth.random_dot(W, H, int(kind[3:]), seed)
     return L, R
@@ -72,6 +76,22 @@ def test_volumes_and_maps(fbs, oracle_lib, case):
     # fbs_compute gives the same bytes as the debug path
     out2 = m.compute(Ld, Rd).cpu().numpy()
     assert np.array_equal(out2.view(np.uint32), out.view(np.uint32))
+    if name == "textureless":  # exercises every denominator form, with the EMPTY test on
+        import os
+        os.environ["FBS_EMPTY_FORM"] = "1"
+        try:
+            me = fbs.FBS(W, H, d_min, d_max, rho, gd, gr)
+        finally:
+            del os.environ["FBS_EMPTY_FORM"]
+        me.profile_enable(1)
+        out3 = me.compute(Ld, Rd).cpu().numpy()
+        forms = me.tile_stats()
+        me.profile_enable(0)
+        assert min(forms.values()) > 0, forms
+        assert np.array_equal(out3.view(np.uint32), out.view(np.uint32))
+        _, _, al3, ar3 = (v.cpu().numpy() for v in me.volumes(Ld, Rd))
+        assert np.array_equal(al3.view(np.uint32), al.view(np.uint32))
+        assert np.array_equal(ar3.view(np.uint32), ar.view(np.uint32))
     # every disagreement was checked to be an oracle near-tie (gap < 1e-5); scenes
     # with textureless layers have many exact ties (perfect correlations at
     # several d), so the count is reported, not bounded
