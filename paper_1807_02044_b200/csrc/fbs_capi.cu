@@ -177,8 +177,9 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
   }
   // opt-in shared memory for every aggregation variant
 #define FBS_SMEM_ATTR(RR) \
-  cudaFuncSetAttribute(k_agg<RR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(AggSmem<RR>)); \
-  cudaFuncSetAttribute(k_agg<RR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(AggSmem<RR>));
+  cudaFuncSetAttribute(k_agg<RR, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(AggSmem<RR>)); \
+  cudaFuncSetAttribute(k_agg<RR, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(AggSmem<RR>)); \
+  cudaFuncSetAttribute(k_agg<RR, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(AggSmem<RR>));
   FBS_SMEM_ATTR(0) FBS_SMEM_ATTR(1) FBS_SMEM_ATTR(2) FBS_SMEM_ATTR(3) FBS_SMEM_ATTR(4)
   FBS_SMEM_ATTR(5) FBS_SMEM_ATTR(6)
 #undef FBS_SMEM_ATTR
@@ -239,10 +240,12 @@ static void launch_agg(const fbs_ctx* h, const AggArgs& a, int ty1, cudaStream_t
   switch (h->R) {
 #define FBS_CASE(RR) \
   case RR:                                                                                        \
-    if (h->empty_form)                                                                            \
-      launch_pdl(k_agg<RR, true>, grid, dim3(AggGeom<RR>::THREADS), sizeof(AggSmem<RR>), s, a);   \
-    else                                                                                          \
-      launch_pdl(k_agg<RR, false>, grid, dim3(AggGeom<RR>::THREADS), sizeof(AggSmem<RR>), s, a);  \
+    if (a.exportR) /* debug export (results identical to both production variants) */                 \
+      launch_pdl(k_agg<RR, false, true>, grid, dim3(AggGeom<RR>::THREADS), sizeof(AggSmem<RR>), s, a);   \
+    else if (h->empty_form)                                                                             \
+      launch_pdl(k_agg<RR, true, false>, grid, dim3(AggGeom<RR>::THREADS), sizeof(AggSmem<RR>), s, a);   \
+    else                                                                                                \
+      launch_pdl(k_agg<RR, false, false>, grid, dim3(AggGeom<RR>::THREADS), sizeof(AggSmem<RR>), s, a);  \
     break;
     FBS_CASE(0) FBS_CASE(1) FBS_CASE(2) FBS_CASE(3) FBS_CASE(4) FBS_CASE(5) FBS_CASE(6)
 #undef FBS_CASE

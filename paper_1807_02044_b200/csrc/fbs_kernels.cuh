@@ -619,7 +619,9 @@ __device__ __forceinline__ unsigned long long wta_butterfly16(unsigned long long
 // code generated for the FAST stream: measured 3.5 % slower at Teddy, 19 %
 // faster on KITTI-shaped streams with textureless frames (an in-kernel switch
 // between both bodies compiled 20 % slower still).  Bit-identical results.
-template <int R, bool EMPTY>
+// EXPORT: the debug export of the right aggregated volume is compiled in (its
+// store loop alone costs the production kernel ~1 %).
+template <int R, bool EMPTY, bool EXPORT>
 __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(const AggArgs a) {
   constexpr int kPY = AggGeom<R>::PY;
   constexpr int kTY = AggGeom<R>::TY;
@@ -767,8 +769,8 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
           *reinterpret_cast<float4*>(vrow(pyl) + px * kDB + 4 * dq) = agg;
         else if (x < a.W && y < a.H)
           *reinterpret_cast<float4*>(a.aggL + (((size_t)y * a.nblk + b) * a.W + x) * kDB + 4 * dq) = agg;
-      } else if (a.exportR && x < a.W && y >= a.r0 && y < a.r1) {
-        float* er = a.exportR + ((size_t)y * a.W + x) * a.D;
+      } else if ((EXPORT ? a.exportR : nullptr) && x < a.W && y >= a.r0 && y < a.r1) {
+        float* er = (EXPORT ? a.exportR : nullptr) + ((size_t)y * a.W + x) * a.D;
         const float av[4] = {agg.x, agg.y, agg.z, agg.w};
 #pragma unroll
         for (int tt = 0; tt < 4; ++tt)
@@ -821,13 +823,13 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
             *reinterpret_cast<float4*>(a.aggL + (((size_t)y * a.nblk + b) * a.W + x) * kDB + 4 * dq) =
                 make_float4(kSent, kSent, kSent, kSent);
         }
-      } else if (side == 1 && a.exportR) {
+      } else if (side == 1 && (EXPORT ? a.exportR : nullptr)) {
 #pragma unroll 1
         for (int s2 = 0; s2 < kPX * HPY; ++s2) {
           const int y = sy + py0 + s2 / kPX, x = sx + s2 % kPX;
           if (x < a.W && y >= a.r0 && y < a.r1)
             for (int tt = 0; tt < 4; ++tt)
-              if (di0 + tt < a.D) a.exportR[((size_t)y * a.W + x) * a.D + di0 + tt] = kSent;
+              if (di0 + tt < a.D) (EXPORT ? a.exportR : nullptr)[((size_t)y * a.W + x) * a.D + di0 + tt] = kSent;
         }
       }
       // no keys: zero keys leave the running best unchanged

@@ -56,7 +56,7 @@ def sass_of(function: str) -> str:
 def test_sass_uses_ffma2():
     """The aggregation inner loop issues FFMA2 with a broadcast scalar weight
     (the radius-4 variant: 9 taps x 4 pixels per weight row)."""
-    out = sass_of("_ZN3fbs5k_aggILi4ELb0EEEvNS_7AggArgsE")
+    out = sass_of("_ZN3fbs5k_aggILi4ELb0ELb0EEEvNS_7AggArgsE")
     assert out.count("FFMA2") >= 24 * 81  # 4x6 px x 81 taps: the FMA stream is fully unrolled
     assert re.search(r"FFMA2 R\d+, R\d+\.F32, R\d+\.F32x2", out)
     cost = sass_of("_ZN3fbs6k_costENS_8CostArgsE")
