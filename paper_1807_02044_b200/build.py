@@ -12,7 +12,7 @@ DEPS = SRC + [os.path.join(HERE, "csrc", "fbs_kernels.cuh"), os.path.join(ROOT, 
 OUT = os.path.join(HERE, "libfbs.so")
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", "--split-compile=0"]
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
