@@ -6,7 +6,7 @@
  *
  *   NCC matching cost      Eq.(1)-(3)   P:L66-84   (block statistics pre-computed)
  *   twin cost volumes      P:L86, P:L185           (left (u,v,d) == right (u-d,v,d))
- *   bilateral aggregation  Eq.(6)-(8)   P:L118-132 (ω_d, ω_r tables pre-computed)
+ *   bilateral aggregation  Eq.(6)-(8)   P:L118-132 (ω_d ω_r pre-computed as exponent constants)
  *   winner-take-all        P:L140, P:L201          (highest aggregated NCC over [d_min, d_max])
  *   left-right consistency Eq.(9)       P:L148-153 (left image is the reference)
  *   parabola subpixel      Eq.(10)
@@ -66,7 +66,7 @@ typedef struct fbs_ctx fbs_ctx;
 typedef struct CUstream_st* fbs_stream_t;
 
 /*
- * fbs_create — validate parameters, build the ω_d / ω_r tables (Eq.(7)(8),
+ * fbs_create — validate parameters, build the ω_d / ω_r exponent constants (Eq.(7)(8),
  * P:L199 "pre-calculated"), allocate all scratch on the current device.
  *   W, H          frame size in pixels (>= 3 each)
  *   d_min, d_max  inclusive disparity search range, 0 <= d_min < d_max
