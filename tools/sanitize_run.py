@@ -16,3 +16,17 @@ for rho in (0, 3, 6):
     m = fbs.FBS(cfg.W, cfg.H, cfg.d_min, cfg.d_max, rho, cfg.gamma_d, cfg.gamma_r)
     out = m.compute(torch.from_numpy(L).cuda(), torch.from_numpy(R).cuda()); torch.cuda.synchronize()
     print("rho", rho, float((out >= 0).float().mean()))
+# the EMPTY-form instantiation on the textureless-heavy KITTI frame, and the
+# debug-export instantiation
+os.environ["FBS_EMPTY_FORM"] = "1"
+cfg = synth.CONFIGS["kitti"]
+L, R = synth.frame(cfg, 1)
+m = fbs.FBS(cfg.W, cfg.H, cfg.d_min, cfg.d_max, cfg.radius, cfg.gamma_d, cfg.gamma_r)
+out = m.compute(torch.from_numpy(L).cuda(), torch.from_numpy(R).cuda()); torch.cuda.synchronize()
+print("kitti empty-form", float((out >= 0).float().mean()))
+del os.environ["FBS_EMPTY_FORM"]
+cfg = synth.CONFIGS["synthetic"]
+L, R = synth.frame(cfg, 0)
+m = fbs.FBS(cfg.W, cfg.H, cfg.d_min, cfg.d_max, cfg.radius, cfg.gamma_d, cfg.gamma_r)
+vols = m.volumes(torch.from_numpy(L).cuda(), torch.from_numpy(R).cuda()); torch.cuda.synchronize()
+print("export", [float(v.float().mean()) for v in vols])
