@@ -63,7 +63,10 @@ struct AggGeom {
 constexpr int kTYMax = kPYMax * 2;                // tallest CTA tile of any radius
 __host__ __device__ constexpr int agg_tile_h(int R) { return (R >= 6 ? 4 : kPYMax) * 2; }
 
-constexpr int kCX = 64;          // cost kernel: pixels per CTA (multiple of 32)
+#ifndef FBS_KCX
+#define FBS_KCX 64
+#endif
+constexpr int kCX = FBS_KCX;     // cost kernel: pixels per CTA (multiple of 32)
 // Padded guide images for k_agg (written by k_cost): i(q) as a float, with an
 // R-pixel margin of kGuideUndef outside the frame.  A pixel whose own block is
 // undefined stores i + kGuideFlag: as a tap q it is >= 2^23 - 255 away from any
