@@ -253,7 +253,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         return None
     # ---- roofline of the dominant kernel (aggregation + WTA, both sides in one launch) ----
     peak, peak_src = load_peak_fp32()
-    agg_ms = stage_ms["agg"] / max(1, nprof)
+    agg_ms = stage_ms["fbs"] / max(1, nprof)
     if banded:
         rows = fdist.band_range(cfg.H, rank, world)
         frac_rows = (rows[1] - rows[0]) / cfg.H
@@ -267,7 +267,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             "avg_launch_ms": round(agg_ms, 5),
             "timing": "k_agg launch duration from CUDA events on the launching stream around each "
                       "launch, in a profiled pass of the same workload right after the timed steps",
-            "share_of_step": round(stage_ms["agg"] / tot_stage, 3) if tot_stage else None,
+            "share_of_step": round(stage_ms["fbs"] / tot_stage, 3) if tot_stage else None,
             "stage_ms_per_frame": {k: round(v / max(1, nprof), 5) for k, v in stage_ms.items()},
             "peak_source": f"148 SM x 128 FP32 lanes x 2 x {peak_src} (nominal); "
                            "FFMA2 microbenchmark 66.9 TFLOP/s (DESIGN.md §6)",

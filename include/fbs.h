@@ -147,18 +147,23 @@ int fbs_compute_host_batch(fbs_ctx* h, const uint8_t* left, const uint8_t* right
                            float* disp_out, fbs_stream_t stream);
 
 /*
- * fbs_debug_volumes — test-only export of the intermediate volumes, each
- * device float [H][W][D] indexed ((v*W+u)*D + d-d_min), FBS_SENTINEL where
- * undefined:
+ * fbs_debug_volumes — test-only: one fbs_compute that also exports the
+ * intermediate volumes, each device float [H][W][D] indexed
+ * ((v*W+u)*D + d-d_min), FBS_SENTINEL where undefined:
  *   cost_l  c(u,v,d) of Eq.(1) (left reference)
  *   cost_r  the right-reference twin, cost_r(u-d,v,d) == cost_l(u,v,d)
  *   agg_l   Eq.(6) on cost_l guided by the left image
  *   agg_r   Eq.(6) on cost_r guided by the right image
- * Any output may be NULL.  Values are exactly those the production kernels
- * compute.  Asynchronous.
+ * and the results of that same launch:
+ *   disp_out        device float [H][W] final map
+ *   disp_l, disp_r  device int32 [H][W] integer WTA maps (-1 = INVALID)
+ * Any output may be NULL.  The exporting kernel is a separate instantiation of
+ * the production kernel (the same arithmetic plus stores); the GPU tests check
+ * that its maps are bit-identical to fbs_compute's.  Asynchronous.
  */
 int fbs_debug_volumes(fbs_ctx* h, const uint8_t* left, const uint8_t* right, float* cost_l,
-                      float* cost_r, float* agg_l, float* agg_r, fbs_stream_t stream);
+                      float* cost_r, float* agg_l, float* agg_r, float* disp_out, int32_t* disp_l,
+                      int32_t* disp_r, fbs_stream_t stream);
 
 /*
  * fbs_debug_select — test-only: WTA on two given aggregated volumes (device

@@ -28,7 +28,7 @@ EXPORTS = ("fbs_create", "fbs_destroy", "fbs_last_error", "fbs_compute", "fbs_co
            "fbs_compute_batch", "fbs_compute_host", "fbs_compute_host_batch", "fbs_debug_volumes", "fbs_debug_select",
            "fbs_debug_maps", "fbs_stats", "fbs_profile_enable", "fbs_profile_read", "fbs_tile_stats")
 FBS_NSTAGES = 3
-STAGES = ("cost", "agg", "finalize")
+STAGES = ("prep", "fbs", "finalize")
 
 _lib = None
 
@@ -59,7 +59,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.fbs_compute_batch.argtypes = [P, P, P, I, P, P]
     lib.fbs_compute_host.argtypes = [P, P, P, P, P]
     lib.fbs_compute_host_batch.argtypes = [P, P, P, I, P, P]
-    lib.fbs_debug_volumes.argtypes = [P, P, P, P, P, P, P, P]
+    lib.fbs_debug_volumes.argtypes = [P, P, P, P, P, P, P, P, P, P, P]
     lib.fbs_debug_select.argtypes = [P, P, P, P, P, P, P]
     lib.fbs_debug_maps.argtypes = [P, P, P, P, P, P, P]
     lib.fbs_stats.argtypes = [P, ctypes.POINTER(I)]
@@ -137,9 +137,10 @@ def fbs_compute_host_batch(h, left, right, n: int, disp_out, stream=None) -> Non
 
 
 def fbs_debug_volumes(h, left, right, cost_l=None, cost_r=None, agg_l=None, agg_r=None,
-                      stream=None) -> None:
+                      disp_out=None, disp_l=None, disp_r=None, stream=None) -> None:
     _check(load_library().fbs_debug_volumes(h, _ptr(left), _ptr(right), _ptr(cost_l), _ptr(cost_r),
-                                            _ptr(agg_l), _ptr(agg_r), _stream(stream)))
+                                            _ptr(agg_l), _ptr(agg_r), _ptr(disp_out), _ptr(disp_l),
+                                            _ptr(disp_r), _stream(stream)))
 
 
 def fbs_debug_select(h, agg_l, agg_r, disp_l=None, disp_r=None, disp_out=None, stream=None) -> None:
@@ -205,77 +206,102 @@ class FBS:
         except Exception:
             pass
 
-    def _chk(self, *ts):
-        for t in ts:
-            if t is not None:
-                assert t.is_cuda and t.is_contiguous(), "device, contiguous tensors required"
+    def _chk_pair(self, left, right, n=None, host=False):
+        """Validate an input pair: uint8, contiguous, [H, W] (or [n, H, W]), on the
+        handle's device (or on the host for the *_host calls)."""
+        import torch
+        shape = (self.H, self.W) if n is None else (n, self.H, self.W)
+        for name, t in (("left", left), ("right", right)):
+            if not isinstance(t, torch.Tensor) or t.dtype != torch.uint8 or not t.is_contiguous():
+                raise ValueError(f"{name}: expected a contiguous uint8 tensor")
+            if tuple(t.shape) != shape:
+                raise ValueError(f"{name}: expected shape {shape}, got {tuple(t.shape)}")
+            if host and t.is_cuda:
+                raise ValueError(f"{name}: expected a host tensor")
+            if not host and (not t.is_cuda or t.device != self.device):
+                raise ValueError(f"{name}: expected a tensor on {self.device}")
+
+    def _out(self, out, shape, dtype=None, host=False):
+        import torch
+        dtype = dtype or torch.float32
+        if out is None:
+            if host:
+                return torch.empty(shape, dtype=dtype, pin_memory=True)
+            return torch.empty(shape, dtype=dtype, device=self.device)
+        if out.dtype != dtype or tuple(out.shape) != tuple(shape) or not out.is_contiguous():
+            raise ValueError(f"out: expected a contiguous {dtype} tensor of shape {tuple(shape)}")
+        if host == out.is_cuda or (not host and out.device != self.device):
+            raise ValueError("out: on the wrong device")
+        return out
 
     def compute(self, left, right, out=None, stream=None):
-        import torch
-        self._chk(left, right)
-        if out is None:
-            out = torch.empty((self.H, self.W), dtype=torch.float32, device=left.device)
+        self._chk_pair(left, right)
+        out = self._out(out, (self.H, self.W))
         fbs_compute(self.h, left, right, out, stream)
         return out
 
     def compute_rows(self, left, right, r0: int, r1: int, out=None, stream=None):
-        import torch
-        self._chk(left, right)
-        if out is None:
-            out = torch.empty((r1 - r0, self.W), dtype=torch.float32, device=left.device)
+        self._chk_pair(left, right)
+        if not 0 <= r0 < r1 <= self.H:
+            raise ValueError("compute_rows: need 0 <= r0 < r1 <= H")
+        out = self._out(out, (r1 - r0, self.W))
         fbs_compute_rows(self.h, left, right, r0, r1, out, stream)
         return out
 
     def compute_batch(self, left, right, out=None, stream=None):
-        import torch
-        self._chk(left, right)
         n = left.shape[0]
-        if out is None:
-            out = torch.empty((n, self.H, self.W), dtype=torch.float32, device=left.device)
+        self._chk_pair(left, right, n=n)
+        out = self._out(out, (n, self.H, self.W))
         fbs_compute_batch(self.h, left, right, n, out, stream)
         return out
 
     def compute_host(self, left, right, out=None, stream=None):
-        import torch
-        if out is None:
-            out = torch.empty((self.H, self.W), dtype=torch.float32, pin_memory=True)
+        self._chk_pair(left, right, host=True)
+        out = self._out(out, (self.H, self.W), host=True)
         fbs_compute_host(self.h, left, right, out, stream)
         return out
 
     def compute_host_batch(self, left, right, out=None, stream=None):
         """left/right: host uint8 [n][H][W] (pinned); returns host float [n][H][W]."""
-        import torch
-        if left.is_cuda or right.is_cuda or tuple(left.shape[1:]) != (self.H, self.W) or left.shape != right.shape:
-            raise ValueError("compute_host_batch: expected host uint8 [n][H][W] pairs")
-        if left.dtype != torch.uint8 or not left.is_contiguous() or not right.is_contiguous():
-            raise ValueError("compute_host_batch: expected contiguous uint8 tensors")
         n = left.shape[0]
-        if out is None:
-            out = torch.empty((n, self.H, self.W), dtype=torch.float32, pin_memory=True)
+        self._chk_pair(left, right, n=n, host=True)
+        out = self._out(out, (n, self.H, self.W), host=True)
         fbs_compute_host_batch(self.h, left, right, n, out, stream)
         return out
 
-    def volumes(self, left, right, stream=None):
+    def volumes(self, left, right, stream=None, maps=False):
+        """Debug export: cost_l, cost_r, agg_l, agg_r ([H][W][D], SENT = undefined);
+        with maps=True also (disp, d_L, d_R) of the same (exporting) launch."""
         import torch
+        self._chk_pair(left, right)
         shp = (self.H, self.W, self.D)
-        vols = [torch.empty(shp, dtype=torch.float32, device=left.device) for _ in range(4)]
-        fbs_debug_volumes(self.h, left, right, *vols, stream=stream)
-        return vols
+        vols = [torch.empty(shp, dtype=torch.float32, device=self.device) for _ in range(4)]
+        out = dl = dr = None
+        if maps:
+            out = torch.empty((self.H, self.W), dtype=torch.float32, device=self.device)
+            dl = torch.empty((self.H, self.W), dtype=torch.int32, device=self.device)
+            dr = torch.empty_like(dl)
+        fbs_debug_volumes(self.h, left, right, *vols, disp_out=out, disp_l=dl, disp_r=dr, stream=stream)
+        return (vols, (out, dl, dr)) if maps else vols
 
     def maps(self, left, right, stream=None):
         import torch
-        out = torch.empty((self.H, self.W), dtype=torch.float32, device=left.device)
-        dl = torch.empty((self.H, self.W), dtype=torch.int32, device=left.device)
+        self._chk_pair(left, right)
+        out = torch.empty((self.H, self.W), dtype=torch.float32, device=self.device)
+        dl = torch.empty((self.H, self.W), dtype=torch.int32, device=self.device)
         dr = torch.empty_like(dl)
         fbs_debug_maps(self.h, left, right, out, dl, dr, stream)
         return out, dl, dr
 
     def select(self, agg_l, agg_r, stream=None):
         import torch
-        out = torch.empty((self.H, self.W), dtype=torch.float32, device=agg_l.device)
-        dl = torch.empty((self.H, self.W), dtype=torch.int32, device=agg_l.device)
+        for t in (agg_l, agg_r):
+            if t.dtype != torch.float32 or tuple(t.shape) != (self.H, self.W, self.D) or not t.is_cuda:
+                raise ValueError("select: expected device float32 [H, W, D] volumes")
+        out = torch.empty((self.H, self.W), dtype=torch.float32, device=self.device)
+        dl = torch.empty((self.H, self.W), dtype=torch.int32, device=self.device)
         dr = torch.empty_like(dl)
-        fbs_debug_select(self.h, agg_l, agg_r, dl, dr, out, stream)
+        fbs_debug_select(self.h, agg_l.contiguous(), agg_r.contiguous(), dl, dr, out, stream)
         return out, dl, dr
 
     def profile_enable(self, n: int):

@@ -1,11 +1,13 @@
 // fbs_capi.cu — C ABI of libfbs.so (declared in include/fbs.h).
 //
-// Host side: parameter validation, ω_d / ω_r tables (Eq.(7)(8), built in
-// double and rounded once to fp32, "pre-calculated"), scratch
-// allocation, and the launch sequence per frame (3 launches):
-//   k_cost      block statistics + twin cost volumes, both sides   Eq.(1)-(3)
-//   k_agg       aggregation + WTA, both sides                      Eq.(6)-(8)
-//   k_finalize  LRC + subpixel -> disp_out                         Eq.(9)(10)
+// Host side: parameter validation, the ω_d / ω_r exponent constants (Eq.(7)(8),
+// built in double and rounded once to fp32, "pre-calculated"), scratch
+// allocation, TMA descriptors, and the launch sequence per batch of frames
+// (3 launches, programmatic dependent launch between them):
+//   k_prep   block statistics, packed columns, guides, masks   Eq.(2)(3)
+//   k_fbs    twin NCC costs in shared memory + aggregation    Eq.(1); Eq.(6)-(8)
+//            + WTA, both sides, all frames of the batch
+//   k_final  LRC + subpixel -> disp_out                        Eq.(9)(10)
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -14,48 +16,48 @@
 #include <string>
 #include <utility>
 
+#include <cuda.h>
+
 #include "../../include/fbs.h"
-#include "fbs_kernels.cuh"
+#include "fbs_fused.cuh"
 
 using namespace fbs;
 
 struct fbs_ctx {
-  int W, H, d_min, d_max, D, nblk, R, Wv, Hv;
+  WalkArgs wa;  // tensor maps, geometry and the Eq.(7)(8) constants (first: 64-B aligned)
+  int W, H, d_min, d_max, D, nblk, R;
   float sigma_s, sigma_r;
-  int device;
-  // Eq.(7)(8) in the exponent form k_agg evaluates: w' = 2^(cd(dx,dy) + nkr Δ²)
-  float cd[(2 * kMaxRadius + 1) * (2 * kMaxRadius + 1)];
-  float nkr;
-  // scratch
-  uint32_t *bitsL, *bitsR;
-  float *gpadL, *gpadR;    // padded guide images for k_agg (k_cost), [guide_rows][Wg]
-  int Wg;
-  bool empty_form;         // k_agg<R, true>: GENERAL units test for EMPTY (FBS_EMPTY_FORM=1 at create)
-  int Wb;
-  float *volL, *volR;
-  int32_t *dL, *dR;
-  float* aggL;       // left aggregated costs [H][nblk][W][64] (k_agg -> k_finalize)
-  float4* agg3;      // one d-block: (c(d*-1), c(d*), c(d*+1)) per left pixel [H][W] (k_agg -> k_finalize)
-  uint8_t *hL, *hR;  // device staging for fbs_compute_host[_batch]: two frame slots each
+  int device, num_sms;
+  int fcap;  // frames per launch (scratch is sized for fcap frames)
+  int Wp, Wg, GR, Wb, TY, TX;
+  size_t gfs;  // guide frame stride (floats)
+  // scratch (fcap frames each)
+  uint32_t* P[2];
+  int2* SR[2];
+  float* G[2];
+  uint32_t* bits[2];
+  int32_t* dmap[2];
+  float4* agg3;
+  unsigned long long* keys;
+  // host path (fbs_compute_host[_batch]): two frame slots each, created on first use
+  bool staging_ready;
+  uint8_t *hL, *hR;
   float* hOut;
-  cudaStream_t cs_in, cs_out;          // copy streams of the host path (created on first use)
-  cudaEvent_t ev_in[2], ev_done[2], ev_out[2];
-  unsigned long long* tile_stats;  // device [4] FAST/EDGE/GENERAL/EMPTY, counting when prof_ev is set
+  cudaStream_t cs_in, cs_out;
+  cudaEvent_t ev_entry, ev_in[2], ev_done[2], ev_out[2];
+  unsigned long long* tile_stats;  // device [4] FAST/EDGE/GENERAL/EMPTY, counting while profiling
   int launches;
-  // live profiling (fbs_profile_enable): kEv events per frame
-  cudaEvent_t* prof_ev;
+  cudaEvent_t* prof_ev;  // live profiling (fbs_profile_enable): kEv events per call
   int prof_cap, prof_n;
 };
 
 static thread_local std::string g_err;
-
 static constexpr int kEv = FBS_NSTAGES + 1;
 
 static int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
 }
-
 static int cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) return fail(FBS_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
   return FBS_OK;
@@ -63,29 +65,115 @@ static int cuda_check(cudaError_t e, const char* what) {
 
 extern "C" const char* fbs_last_error(void) { return g_err.c_str(); }
 
-static void free_host_path(fbs_ctx* h) {
-  if (h->cs_in) {
-    cudaStreamDestroy(h->cs_in);
-    cudaStreamDestroy(h->cs_out);
-    for (int k = 0; k < 2; ++k) {
-      cudaEventDestroy(h->ev_in[k]);
-      cudaEventDestroy(h->ev_done[k]);
-      cudaEventDestroy(h->ev_out[k]);
-    }
-    h->cs_in = h->cs_out = nullptr;
+// ---------------------------------------------------------------------------
+// Geometry per radius (the walker's compile-time traits)
+template <int R>
+static void geo_of(int& TX, int& TY, size_t& smem) {
+  TX = WGeo<R>::TX;
+  TY = WGeo<R>::TY;
+  smem = sizeof(WSmem<R>) + 128;  // + alignment slack of the dynamic base
+}
+static void geometry(int R, int& TX, int& TY, size_t& smem) {
+  switch (R) {
+#define FBS_GEO(RR) \
+  case RR: geo_of<RR>(TX, TY, smem); break;
+    FBS_GEO(0) FBS_GEO(1) FBS_GEO(2) FBS_GEO(3) FBS_GEO(4) FBS_GEO(5) FBS_GEO(6)
+#undef FBS_GEO
   }
+}
+
+// ---------------------------------------------------------------------------
+// TMA descriptors (driver entry point, no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (EncodeTiledFn) nullptr;
+    return (EncodeTiledFn)p;
+  }();
+  return fn;
+}
+
+// 3-D map over [F][rows][cols] elements of esize bytes (row pitch `pitch` elements);
+// out-of-range elements read as zero (an undefined block / no packed column).
+static bool make_map(CUtensorMap* m, void* base, CUtensorMapDataType dt, int esize, int cols, int rows, int pitch,
+                     int frames, int box_cols, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)frames};
+  const cuuint64_t strides[2] = {(cuuint64_t)pitch * esize, (cuuint64_t)pitch * esize * rows};
+  const cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, dt, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int R>
+static bool make_maps(fbs_ctx* h) {
+  using G = WGeo<R>;
+  bool ok = true;
+  for (int im = 0; im < 2; ++im) {
+    ok &= make_map(&h->wa.tmPs[im], h->P[im], CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, h->W, h->H, h->Wp, h->fcap, G::SPC,
+                   G::SROWS);
+    ok &= make_map(&h->wa.tmPo[im], h->P[im], CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, h->W, h->H, h->Wp, h->fcap, G::OPC,
+                   G::SROWS);
+    // (S, r) pairs as 32-bit words: x coordinates are doubled
+    ok &= make_map(&h->wa.tmSs[im], h->SR[im], CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, 2 * h->W, h->H, 2 * h->Wp, h->fcap,
+                   2 * G::SSC, G::SROWS);
+    ok &= make_map(&h->wa.tmSo[im], h->SR[im], CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, 2 * h->W, h->H, 2 * h->Wp, h->fcap,
+                   2 * G::OSC, G::SROWS);
+    ok &= make_map(&h->wa.tmG[im], h->G[im], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, h->Wg, h->GR, h->Wg, h->fcap, G::GWS,
+                   G::GH);
+  }
+  return ok;
+}
+static bool build_maps(fbs_ctx* h) {
+  switch (h->R) {
+#define FBS_MAPS(RR) \
+  case RR: return make_maps<RR>(h);
+    FBS_MAPS(0) FBS_MAPS(1) FBS_MAPS(2) FBS_MAPS(3) FBS_MAPS(4) FBS_MAPS(5) FBS_MAPS(6)
+#undef FBS_MAPS
+  }
+  return false;
+}
+
+// ---------------------------------------------------------------------------
+static void free_host_path(fbs_ctx* h) {
+  if (h->cs_in) cudaStreamDestroy(h->cs_in);
+  if (h->cs_out) cudaStreamDestroy(h->cs_out);
+  cudaEvent_t evs[] = {h->ev_entry, h->ev_in[0], h->ev_in[1], h->ev_done[0], h->ev_done[1], h->ev_out[0], h->ev_out[1]};
+  for (cudaEvent_t e : evs)
+    if (e) cudaEventDestroy(e);
+  void* ptrs[] = {h->hL, h->hR, h->hOut};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  h->cs_in = h->cs_out = nullptr;
+  h->ev_entry = h->ev_in[0] = h->ev_in[1] = h->ev_done[0] = h->ev_done[1] = h->ev_out[0] = h->ev_out[1] = nullptr;
+  h->hL = h->hR = nullptr;
+  h->hOut = nullptr;
+  h->staging_ready = false;
 }
 
 static void free_all(fbs_ctx* h) {
   free_host_path(h);
-  void* ptrs[] = {h->gpadL, h->gpadR, h->bitsL, h->bitsR, h->volL, h->volR, h->dL, h->dR, h->aggL, h->agg3, h->hL, h->hR, h->hOut,
-                  h->tile_stats};
+  void* ptrs[] = {h->P[0], h->P[1], h->SR[0], h->SR[1], h->G[0], h->G[1], h->bits[0], h->bits[1],
+                  h->dmap[0], h->dmap[1], h->agg3, h->keys, h->tile_stats};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
 
-extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, float sigma_s,
-                               float sigma_r) {
+static size_t frame_bytes(const fbs_ctx* h) {
+  const size_t npix = (size_t)h->W * h->H;
+  return 2 * ((size_t)h->H * h->Wp * 12 + (size_t)h->GR * h->Wg * 4 + (size_t)h->H * h->Wb * 4 + npix * 4) +
+         npix * 16 + (h->nblk > 1 ? 2 * npix * 8 : 0);
+}
+
+extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, float sigma_s, float sigma_r) {
   g_err.clear();
   if (W < 3 || H < 3) {
     fail(FBS_E_DIM, "fbs_create: W and H must be >= 3 (one 3x3 NCC block)");
@@ -104,8 +192,12 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
     fail(FBS_E_UNSUPPORTED, "fbs_create: radius > FBS_MAX_RADIUS");
     return nullptr;
   }
-  if ((long long)(d_max - d_min + 1) > 4096) {
-    fail(FBS_E_UNSUPPORTED, "fbs_create: more than 4096 disparities");
+  if ((long long)d_max - d_min + 1 > 4096 || W > (1 << 20) || H > (1 << 20)) {
+    fail(FBS_E_UNSUPPORTED, "fbs_create: more than 4096 disparities or a side above 2^20 pixels");
+    return nullptr;
+  }
+  if (!encode_fn()) {
+    fail(FBS_E_CUDA, "fbs_create: cuTensorMapEncodeTiled is not available from the driver");
     return nullptr;
   }
   fbs_ctx* h = new (std::nothrow) fbs_ctx();
@@ -113,45 +205,48 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
     fail(FBS_E_OOM, "fbs_create: host allocation failed");
     return nullptr;
   }
-  std::memset(h, 0, sizeof(*h));
+  std::memset((void*)h, 0, sizeof(*h));
   h->W = W; h->H = H; h->d_min = d_min; h->d_max = d_max; h->D = d_max - d_min + 1;
   h->nblk = (h->D + kDB - 1) / kDB;
   h->R = radius;
-  h->Wv = (W + kTX - 1) / kTX * kTX + 2 * radius;
-  h->Hv = (H + kTYMax - 1) / kTYMax * kTYMax + kTYMax + 2 * radius;
   h->sigma_s = sigma_s; h->sigma_r = sigma_r;
-  {  // tuning knob for scenes with large textureless regions
-    const char* e = std::getenv("FBS_EMPTY_FORM");
-    h->empty_form = e && e[0] == '1';
-  }
   cudaGetDevice(&h->device);
+  cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
+  size_t smem = 0;
+  geometry(radius, h->TX, h->TY, smem);
+  h->Wp = (W + 3) / 4 * 4;
+  h->Wg = guide_pitch(W, radius);
+  h->GR = guide_rows(H, radius);
+  h->gfs = (size_t)h->GR * h->Wg;
+  h->Wb = (W + 31) / 32 + 1;
+  {  // frames per launch: up to 16, within ~256 MB of per-frame scratch
+    const size_t fb = frame_bytes(h);
+    size_t fc = (256u << 20) / (fb ? fb : 1);
+    h->fcap = (int)(fc < 1 ? 1 : (fc > 16 ? 16 : fc));
+  }
   // Eq.(7): ω_d(dx,dy) = exp(-(dx²+dy²)/γ_d²); Eq.(8): ω_r(Δ) = exp(-Δ²/γ_r²)  (R#10).
-  // k_agg evaluates the product as one power of two: ω_d ω_r = 2^(cd(dx,dy) + nkr Δ²),
+  // k_fbs evaluates the product as one power of two: ω_d ω_r = 2^(cd(dx,dy) + nkr Δ²),
   // cd = -log2(e)(dx²+dy²)/γ_d², nkr = -log2(e)/γ_r² (built in double, rounded once;
   // P:L199 "pre-calculated").
   const int K1 = 2 * radius + 1;
   const double gd = sigma_s, gr = sigma_r, l2e = 1.4426950408889634;
   for (int dy = -radius; dy <= radius; ++dy)
     for (int dx = -radius; dx <= radius; ++dx)
-      h->cd[(dy + radius) * K1 + (dx + radius)] = (float)(-l2e * (double)(dx * dx + dy * dy) / (gd * gd));
-  h->nkr = (float)(-l2e / (gr * gr));
+      h->wa.cd[(dy + radius) * K1 + (dx + radius)] = (float)(-l2e * (double)(dx * dx + dy * dy) / (gd * gd));
+  h->wa.nkr = (float)(-l2e / (gr * gr));
 
-  const size_t npix = (size_t)W * H;
-  const size_t nvol = (size_t)h->Hv * h->Wv * h->nblk * kDB;
+  const size_t F = h->fcap, npix = (size_t)W * H;
+  const size_t np = F * H * h->Wp;
   bool ok = true;
-  h->Wb = (W + kCX - 1) / kCX * (kCX / 32);
-  h->Wg = guide_pitch(W, radius);
-  const size_t ngp = (size_t)guide_rows(H, radius) * h->Wg;
-  ok &= cudaMalloc(&h->gpadL, ngp * 4) == cudaSuccess;
-  ok &= cudaMalloc(&h->gpadR, ngp * 4) == cudaSuccess;
-  ok &= cudaMalloc(&h->bitsL, (size_t)H * h->Wb * 4) == cudaSuccess;
-  ok &= cudaMalloc(&h->bitsR, (size_t)H * h->Wb * 4) == cudaSuccess;
-  ok &= cudaMalloc(&h->volL, nvol * 4) == cudaSuccess;
-  ok &= cudaMalloc(&h->volR, nvol * 4) == cudaSuccess;
-  ok &= cudaMalloc(&h->dL, npix * 4) == cudaSuccess;
-  ok &= cudaMalloc(&h->dR, npix * 4) == cudaSuccess;
-  ok &= cudaMalloc(&h->aggL, npix * h->nblk * kDB * sizeof(float)) == cudaSuccess;
-  ok &= cudaMalloc(&h->agg3, npix * sizeof(float4)) == cudaSuccess;
+  for (int im = 0; im < 2; ++im) {
+    ok &= cudaMalloc(&h->P[im], np * 4) == cudaSuccess;
+    ok &= cudaMalloc(&h->SR[im], np * 8) == cudaSuccess;
+    ok &= cudaMalloc(&h->G[im], F * h->gfs * 4) == cudaSuccess;
+    ok &= cudaMalloc(&h->bits[im], F * H * h->Wb * 4) == cudaSuccess;
+    ok &= cudaMalloc(&h->dmap[im], F * npix * 4) == cudaSuccess;
+  }
+  ok &= cudaMalloc(&h->agg3, F * npix * sizeof(float4)) == cudaSuccess;
+  if (h->nblk > 1) ok &= cudaMalloc(&h->keys, 2 * F * npix * 8) == cudaSuccess;
   ok &= cudaMalloc(&h->tile_stats, 4 * sizeof(unsigned long long)) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
@@ -160,35 +255,48 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
     fail(FBS_E_OOM, "fbs_create: device allocation failed");
     return nullptr;
   }
-  // margins (and never-written rows) of the volumes hold the undefined cost
-  k_fill<<<1184, 256>>>(h->volL, nvol, kUndef);
-  k_fill<<<1184, 256>>>(h->volR, nvol, kUndef);
-  k_fill<<<256, 256>>>(h->gpadL, ngp, kGuideUndef);  // margins: taps outside the frame
-  k_fill<<<256, 256>>>(h->gpadR, ngp, kGuideUndef);
+  for (int im = 0; im < 2; ++im) {
+    k_fill<<<256, 256>>>(h->G[im], F * h->gfs, kGuideUndef);  // margins: taps outside the frame
+    cudaMemset(h->dmap[im], 0xff, F * npix * 4);
+    cudaMemset(h->bits[im], 0, F * H * h->Wb * 4);
+  }
   cudaMemset(h->tile_stats, 0, 4 * sizeof(unsigned long long));
-  cudaMemset(h->dL, 0xff, npix * 4);
-  cudaMemset(h->dR, 0xff, npix * 4);
-  cudaMemset(h->bitsL, 0, (size_t)H * h->Wb * 4);
-  cudaMemset(h->bitsR, 0, (size_t)H * h->Wb * 4);
   if (cuda_check(cudaDeviceSynchronize(), "fbs_create init") != FBS_OK) {
     free_all(h);
     delete h;
     return nullptr;
   }
-  // opt-in shared memory for every aggregation variant
-#define FBS_SMEM_ATTR(RR) \
-  cudaFuncSetAttribute(k_agg<RR, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(AggSmem<RR>)); \
-  cudaFuncSetAttribute(k_agg<RR, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(AggSmem<RR>)); \
-  cudaFuncSetAttribute(k_agg<RR, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(AggSmem<RR>));
-  FBS_SMEM_ATTR(0) FBS_SMEM_ATTR(1) FBS_SMEM_ATTR(2) FBS_SMEM_ATTR(3) FBS_SMEM_ATTR(4)
-  FBS_SMEM_ATTR(5) FBS_SMEM_ATTR(6)
+  if (!build_maps(h)) {
+    free_all(h);
+    delete h;
+    fail(FBS_E_CUDA, "fbs_create: cuTensorMapEncodeTiled rejected a descriptor");
+    return nullptr;
+  }
+  // fixed per instantiation, so setting it per handle never lowers another handle's cap
+  switch (radius) {
+#define FBS_SMEM_ATTR(RR)                                                                                  \
+  case RR:                                                                                                 \
+    cudaFuncSetAttribute(k_fbs<RR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
+    cudaFuncSetAttribute(k_fbs<RR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
+    break;
+    FBS_SMEM_ATTR(0) FBS_SMEM_ATTR(1) FBS_SMEM_ATTR(2) FBS_SMEM_ATTR(3) FBS_SMEM_ATTR(4) FBS_SMEM_ATTR(5)
+    FBS_SMEM_ATTR(6)
 #undef FBS_SMEM_ATTR
-  cudaFuncSetAttribute(k_cost, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cost_smem_bytes(h->nblk));
+  }
   if (cuda_check(cudaGetLastError(), "fbs_create smem attributes") != FBS_OK) {
     free_all(h);
     delete h;
     return nullptr;
   }
+  // constant part of the walker's arguments
+  WalkArgs& a = h->wa;
+  a.W = W; a.H = H; a.D = h->D; a.d_min = d_min; a.d_max = d_max; a.nblk = h->nblk;
+  a.Wb = h->Wb;
+  a.bits[0] = h->bits[0]; a.bits[1] = h->bits[1];
+  a.dmap[0] = h->dmap[0]; a.dmap[1] = h->dmap[1];
+  a.agg3 = h->agg3;
+  a.keys = h->keys;
+  a.nstrips = (W + h->TX - 1) / h->TX;
   return h;
 }
 
@@ -209,14 +317,6 @@ extern "C" void fbs_destroy(fbs_ctx* h) {
 }
 
 // ---------------------------------------------------------------------------
-static void fill_agg_args(const fbs_ctx* h, AggArgs& a) {
-  a.W = h->W; a.H = h->H; a.D = h->D; a.d_min = h->d_min; a.d_max = h->d_max;
-  a.nblk = h->nblk; a.Wv = h->Wv;
-  std::memcpy(a.cd, h->cd, sizeof(a.cd));
-  a.nkr = h->nkr;
-  a.gpadL = h->gpadL; a.gpadR = h->gpadR; a.Wg = h->Wg;
-}
-
 // Launch with programmatic stream serialization (PDL): the kernel may begin
 // while its predecessor drains; it synchronises on it with pdl_wait().
 template <typename... KArgs, typename... Args>
@@ -235,79 +335,72 @@ static cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
-static void launch_agg(const fbs_ctx* h, const AggArgs& a, int ty1, cudaStream_t s) {
-  dim3 grid((h->W + kTX - 1) / kTX, ty1 - a.ty0, 2);
+static cudaError_t launch_walk(const fbs_ctx* h, const WalkArgs& a, bool exp, cudaStream_t s) {
+  const long long g = a.total < h->num_sms ? a.total : h->num_sms;
+  int tx, ty;
+  size_t smem;
+  geometry(h->R, tx, ty, smem);
   switch (h->R) {
-#define FBS_CASE(RR) \
-  case RR:                                                                                        \
-    if (a.exportR) /* debug export (results identical to both production variants) */                 \
-      launch_pdl(k_agg<RR, false, true>, grid, dim3(AggGeom<RR>::THREADS), sizeof(AggSmem<RR>), s, a);   \
-    else if (h->empty_form)                                                                             \
-      launch_pdl(k_agg<RR, true, false>, grid, dim3(AggGeom<RR>::THREADS), sizeof(AggSmem<RR>), s, a);   \
-    else                                                                                                \
-      launch_pdl(k_agg<RR, false, false>, grid, dim3(AggGeom<RR>::THREADS), sizeof(AggSmem<RR>), s, a);  \
-    break;
+#define FBS_CASE(RR)                                                                                 \
+  case RR:                                                                                           \
+    return exp ? launch_pdl(k_fbs<RR, true>, dim3((unsigned)g), dim3(256), smem, s, a)               \
+               : launch_pdl(k_fbs<RR, false>, dim3((unsigned)g), dim3(256), smem, s, a);
     FBS_CASE(0) FBS_CASE(1) FBS_CASE(2) FBS_CASE(3) FBS_CASE(4) FBS_CASE(5) FBS_CASE(6)
 #undef FBS_CASE
   }
+  return cudaErrorInvalidValue;
 }
 
-// Rows [r0, r1) of the output; every stage restricted to the rows it needs.
-static int run_rows(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0, int r1, float* out,
-                    float* aggL_exp, float* aggR_exp, cudaStream_t s) {
-  const int W = h->W, H = h->H, R = h->R;
-  // aggregation tiles are anchored at multiples of the tile height in frame rows, so a
-  // pixel's denominator form never depends on the band; cost rows cover the
-  // tiles' windows (the classification reads validity masks over them too)
-  const int TY = agg_tile_h(R);
+// nf frames (left/right: nf x [H][W] device), output rows [r0, r1) of each into
+// out (nf x [r1-r0][W]); exports (one frame) when expC/expA are set.
+static int run(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int nf, int r0, int r1, float* out,
+               float* const* expC, float* const* expA, cudaStream_t s) {
+  const int W = h->W, H = h->H, R = h->R, TY = h->TY;
+  // walker steps are anchored at multiples of TY in frame rows, so a pixel's
+  // denominator form never depends on the band; cost rows cover their windows
   const int ty0 = r0 / TY, ty1 = (r1 + TY - 1) / TY;
-  const int c0 = std::max(0, ty0 * TY - R), c1 = std::min(H, ty1 * TY + R);  // cost rows
+  const int c0 = std::max(0, ty0 * TY - R), c1 = std::min(H, ty1 * TY + R);
   h->launches = 0;
   cudaEvent_t* ev = nullptr;
   if (h->prof_ev && h->prof_n < h->prof_cap) ev = h->prof_ev + kEv * h->prof_n++;
   if (ev) cudaEventRecord(ev[0], s);
+  cudaError_t e;
   {
-    CostArgs ca;
-    ca.W = W; ca.H = H; ca.D = h->D; ca.d_min = h->d_min; ca.nblk = h->nblk; ca.Wv = h->Wv; ca.R = R;
-    ca.r0 = c0; ca.r1 = c1;
-    ca.L = L; ca.Rimg = Rimg; ca.volL = h->volL; ca.volR = h->volR;
-    ca.bitsL = h->bitsL; ca.bitsR = h->bitsR; ca.Wb = h->Wb;
-    ca.gpadL = h->gpadL; ca.gpadR = h->gpadR; ca.Wg = h->Wg;
-    const size_t smem = cost_smem_bytes(h->nblk);
-    dim3 grd((W + kCX - 1) / kCX, c1 - c0, 2);
-    k_cost<<<grd, 256, smem, s>>>(ca);
+    PrepArgs p;
+    p.W = W; p.H = H; p.Wp = h->Wp; p.Wg = h->Wg; p.Wb = h->Wb; p.R = R; p.y0 = c0; p.y1 = c1;
+    p.img[0] = L; p.img[1] = Rimg;
+    for (int im = 0; im < 2; ++im) { p.P[im] = h->P[im]; p.SR[im] = h->SR[im]; p.G[im] = h->G[im]; p.bits[im] = h->bits[im]; }
+    p.gfs = h->gfs;
+    e = launch_pdl(k_prep, dim3((W + 127) / 128, c1 - c0, 2 * nf), dim3(128), 0, s, p);
+    if (e != cudaSuccess) return cuda_check(e, "k_prep launch");
     h->launches += 1;
   }
   if (ev) cudaEventRecord(ev[1], s);
-  AggArgs a;
-  fill_agg_args(h, a);
-  a.r0 = r0; a.r1 = r1; a.ty0 = ty0;
-  a.volL = h->volL; a.volR = h->volR;
-
-  a.bitsL = h->bitsL; a.bitsR = h->bitsR; a.Wb = h->Wb;
-  a.dL = h->dL; a.dR = h->dR; a.aggL = h->aggL; a.exportR = aggR_exp;
-  // one d-block: the left costs stay on chip and only Eq.(10)'s three are stored
-  // (unless the debug export wants the whole left volume)
-  a.agg3 = (h->nblk == 1 && !aggL_exp) ? h->agg3 : nullptr;
-  a.tile_stats = ev ? h->tile_stats : nullptr;
-  launch_agg(h, a, ty1, s);
-  h->launches += 1;
-  if (ev) cudaEventRecord(ev[2], s);
   {
-    dim3 grd((W + 127) / 128, r1 - r0);
-    launch_pdl(k_finalize, grd, dim3(128), 0, s, (const int32_t*)h->dL, (const int32_t*)h->dR,
-               (const float*)h->aggL, (const float4*)a.agg3, h->nblk, W, r0, r1, h->d_min, h->d_max, out);
+    WalkArgs& a = h->wa;
+    a.r0 = r0; a.r1 = r1;
+    a.ty0 = ty0; a.nty = ty1 - ty0; a.nframes = nf;
+    a.total = (long long)nf * 2 * a.nstrips * a.nty;
+    a.expC[0] = expC ? expC[0] : nullptr; a.expC[1] = expC ? expC[1] : nullptr;
+    a.expA[0] = expA ? expA[0] : nullptr; a.expA[1] = expA ? expA[1] : nullptr;
+    a.tile_stats = ev ? h->tile_stats : nullptr;
+    e = launch_walk(h, a, expC || expA, s);
+    if (e != cudaSuccess) return cuda_check(e, "k_fbs launch");
     h->launches += 1;
   }
+  if (ev) cudaEventRecord(ev[2], s);
+  e = launch_pdl(k_final, dim3((W + 127) / 128, r1 - r0, nf), dim3(128), 0, s, (const int32_t*)h->dmap[0],
+                 (const int32_t*)h->dmap[1], (const float4*)h->agg3, W, H, r0, r1, h->d_min, h->d_max, out);
+  if (e != cudaSuccess) return cuda_check(e, "k_final launch");
+  h->launches += 1;
   if (ev) cudaEventRecord(ev[3], s);
-  if (aggL_exp) k_export_agg<<<1184, 256, 0, s>>>(h->aggL, W, H, h->D, h->nblk, aggL_exp);
   return cuda_check(cudaGetLastError(), "fbs launch");
 }
 
 extern "C" int fbs_compute(fbs_ctx* h, const uint8_t* left, const uint8_t* right, float* disp_out,
                            fbs_stream_t stream) {
   if (!h || !left || !right || !disp_out) return fail(FBS_E_ARG, "fbs_compute: NULL argument");
-  return run_rows(h, left, right, 0, h->H, disp_out, nullptr, nullptr, (cudaStream_t)stream);
+  return run(h, left, right, 1, 0, h->H, disp_out, nullptr, nullptr, (cudaStream_t)stream);
 }
 
 extern "C" int fbs_compute_rows(fbs_ctx* h, const uint8_t* left, const uint8_t* right, int row_begin,
@@ -315,7 +408,7 @@ extern "C" int fbs_compute_rows(fbs_ctx* h, const uint8_t* left, const uint8_t* 
   if (!h || !left || !right || !disp_band) return fail(FBS_E_ARG, "fbs_compute_rows: NULL argument");
   if (row_begin < 0 || row_end > h->H || row_begin >= row_end)
     return fail(FBS_E_ARG, "fbs_compute_rows: need 0 <= row_begin < row_end <= H");
-  return run_rows(h, left, right, row_begin, row_end, disp_band, nullptr, nullptr, (cudaStream_t)stream);
+  return run(h, left, right, 1, row_begin, row_end, disp_band, nullptr, nullptr, (cudaStream_t)stream);
 }
 
 extern "C" int fbs_compute_batch(fbs_ctx* h, const uint8_t* left, const uint8_t* right, int n,
@@ -324,9 +417,10 @@ extern "C" int fbs_compute_batch(fbs_ctx* h, const uint8_t* left, const uint8_t*
   if (n < 1) return fail(FBS_E_ARG, "fbs_compute_batch: n must be >= 1");
   const size_t npix = (size_t)h->W * h->H;
   int launches = 0;
-  for (int i = 0; i < n; ++i) {
-    int rc = run_rows(h, left + i * npix, right + i * npix, 0, h->H, disp_out + i * npix, nullptr,
-                      nullptr, (cudaStream_t)stream);
+  for (int i = 0; i < n; i += h->fcap) {
+    const int m = std::min(h->fcap, n - i);
+    int rc = run(h, left + i * npix, right + i * npix, m, 0, h->H, disp_out + i * npix, nullptr, nullptr,
+                 (cudaStream_t)stream);
     if (rc != FBS_OK) return rc;
     launches += h->launches;
   }
@@ -337,27 +431,39 @@ extern "C" int fbs_compute_batch(fbs_ctx* h, const uint8_t* left, const uint8_t*
 // Host path: frame i's copies in (stream cs_in), compute (caller's stream) and
 // copy out (cs_out) are ordered by events; two staging slots let frame i+1's
 // upload and frame i-1's download run on the copy engines while frame i computes.
+static int host_setup(fbs_ctx* h) {
+  if (h->staging_ready) return FBS_OK;
+  const size_t npix = (size_t)h->W * h->H;
+  bool ok = cudaMalloc(&h->hL, 2 * npix) == cudaSuccess && cudaMalloc(&h->hR, 2 * npix) == cudaSuccess &&
+            cudaMalloc(&h->hOut, 2 * npix * 4) == cudaSuccess;
+  ok = ok && cudaStreamCreateWithFlags(&h->cs_in, cudaStreamNonBlocking) == cudaSuccess &&
+       cudaStreamCreateWithFlags(&h->cs_out, cudaStreamNonBlocking) == cudaSuccess &&
+       cudaEventCreateWithFlags(&h->ev_entry, cudaEventDisableTiming) == cudaSuccess;
+  for (int k = 0; ok && k < 2; ++k)
+    ok = cudaEventCreateWithFlags(&h->ev_in[k], cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&h->ev_done[k], cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&h->ev_out[k], cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    free_host_path(h);  // leaves no half-built state behind
+    return fail(FBS_E_OOM, "fbs_compute_host_batch: staging allocation failed");
+  }
+  h->staging_ready = true;
+  return FBS_OK;
+}
+
 extern "C" int fbs_compute_host_batch(fbs_ctx* h, const uint8_t* left, const uint8_t* right, int n,
                                       float* disp_out, fbs_stream_t stream) {
   if (!h || !left || !right || !disp_out) return fail(FBS_E_ARG, "fbs_compute_host_batch: NULL argument");
   if (n < 1) return fail(FBS_E_ARG, "fbs_compute_host_batch: n must be >= 1");
+  int rc = host_setup(h);
+  if (rc) return rc;
   const size_t npix = (size_t)h->W * h->H;
   cudaStream_t s = (cudaStream_t)stream;
-  if (!h->hL) {
-    bool ok = cudaMalloc(&h->hL, 2 * npix) == cudaSuccess && cudaMalloc(&h->hR, 2 * npix) == cudaSuccess &&
-              cudaMalloc(&h->hOut, 2 * npix * 4) == cudaSuccess;
-    ok = ok && cudaStreamCreateWithFlags(&h->cs_in, cudaStreamNonBlocking) == cudaSuccess &&
-         cudaStreamCreateWithFlags(&h->cs_out, cudaStreamNonBlocking) == cudaSuccess;
-    for (int k = 0; ok && k < 2; ++k)
-      ok = cudaEventCreateWithFlags(&h->ev_in[k], cudaEventDisableTiming) == cudaSuccess &&
-           cudaEventCreateWithFlags(&h->ev_done[k], cudaEventDisableTiming) == cudaSuccess &&
-           cudaEventCreateWithFlags(&h->ev_out[k], cudaEventDisableTiming) == cudaSuccess;
-    if (!ok) {
-      cudaGetLastError();
-      return fail(FBS_E_OOM, "fbs_compute_host_batch: staging allocation failed");
-    }
-  }
-  int rc;
+  // the copy streams start after everything already enqueued on the caller's stream
+  cudaEventRecord(h->ev_entry, s);
+  cudaStreamWaitEvent(h->cs_in, h->ev_entry, 0);
+  cudaStreamWaitEvent(h->cs_out, h->ev_entry, 0);
   for (int i = 0; i < n; ++i) {
     const int k = i & 1;
     uint8_t *dl = h->hL + k * npix, *dr = h->hR + k * npix;
@@ -378,6 +484,8 @@ extern "C" int fbs_compute_host_batch(fbs_ctx* h, const uint8_t* left, const uin
       return rc;
     cudaEventRecord(h->ev_out[k], h->cs_out);
   }
+  // the caller's stream resumes after the last download
+  cudaStreamWaitEvent(s, h->ev_out[(n - 1) & 1], 0);
   if ((rc = cuda_check(cudaStreamSynchronize(h->cs_out), "fbs_compute_host_batch sync"))) return rc;
   return cuda_check(cudaStreamSynchronize(s), "fbs_compute_host_batch sync");
 }
@@ -389,20 +497,23 @@ extern "C" int fbs_compute_host(fbs_ctx* h, const uint8_t* left, const uint8_t* 
 }
 
 extern "C" int fbs_debug_volumes(fbs_ctx* h, const uint8_t* left, const uint8_t* right, float* cost_l,
-                                 float* cost_r, float* agg_l, float* agg_r, fbs_stream_t stream) {
+                                 float* cost_r, float* agg_l, float* agg_r, float* disp_out, int32_t* disp_l,
+                                 int32_t* disp_r, fbs_stream_t stream) {
   if (!h || !left || !right) return fail(FBS_E_ARG, "fbs_debug_volumes: NULL argument");
   cudaStream_t s = (cudaStream_t)stream;
   const size_t npix = (size_t)h->W * h->H;
   float* tmp = nullptr;
-  if (cudaMalloc(&tmp, npix * 4) != cudaSuccess) return fail(FBS_E_OOM, "fbs_debug_volumes: scratch");
-  int rc = run_rows(h, left, right, 0, h->H, tmp, agg_l, agg_r, s);
-  if (rc == FBS_OK) {
-    if (cost_l) k_export_vol<<<1184, 256, 0, s>>>(h->volL, h->W, h->H, h->D, h->nblk, h->Wv, h->R, cost_l);
-    if (cost_r) k_export_vol<<<1184, 256, 0, s>>>(h->volR, h->W, h->H, h->D, h->nblk, h->Wv, h->R, cost_r);
-    rc = cuda_check(cudaGetLastError(), "fbs_debug_volumes export");
+  if (!disp_out && cudaMalloc(&tmp, npix * 4) != cudaSuccess) return fail(FBS_E_OOM, "fbs_debug_volumes: scratch");
+  float* expC[2] = {cost_l, cost_r};
+  float* expA[2] = {agg_l, agg_r};
+  const bool any = cost_l || cost_r || agg_l || agg_r;
+  int rc = run(h, left, right, 1, 0, h->H, disp_out ? disp_out : tmp, any ? expC : nullptr, any ? expA : nullptr, s);
+  if (rc == FBS_OK && disp_l) rc = cuda_check(cudaMemcpyAsync(disp_l, h->dmap[0], npix * 4, cudaMemcpyDeviceToDevice, s), "copy d_L");
+  if (rc == FBS_OK && disp_r) rc = cuda_check(cudaMemcpyAsync(disp_r, h->dmap[1], npix * 4, cudaMemcpyDeviceToDevice, s), "copy d_R");
+  if (tmp) {
+    cudaStreamSynchronize(s);
+    cudaFree(tmp);
   }
-  cudaStreamSynchronize(s);
-  cudaFree(tmp);
   return rc;
 }
 
@@ -412,15 +523,13 @@ extern "C" int fbs_debug_select(fbs_ctx* h, const float* agg_l, const float* agg
   cudaStream_t s = (cudaStream_t)stream;
   const size_t npix = (size_t)h->W * h->H;
   const int nb = (int)((npix + 255) / 256);
-  k_select_wta<<<nb, 256, 0, s>>>(agg_r, h->W, h->H, h->D, h->d_min, h->nblk, h->dR, nullptr);
-  k_select_wta<<<nb, 256, 0, s>>>(agg_l, h->W, h->H, h->D, h->d_min, h->nblk, h->dL, h->aggL);
-  if (disp_out) {
-    dim3 grd((h->W + 127) / 128, h->H);
-    k_finalize<<<grd, 128, 0, s>>>(h->dL, h->dR, h->aggL, nullptr, h->nblk, h->W, 0, h->H, h->d_min, h->d_max,
-                                   disp_out);
-  }
-  if (disp_l) cudaMemcpyAsync(disp_l, h->dL, npix * 4, cudaMemcpyDeviceToDevice, s);
-  if (disp_r) cudaMemcpyAsync(disp_r, h->dR, npix * 4, cudaMemcpyDeviceToDevice, s);
+  k_select_wta<<<nb, 256, 0, s>>>(agg_r, h->W, h->H, h->D, h->d_min, h->dmap[1], nullptr);
+  k_select_wta<<<nb, 256, 0, s>>>(agg_l, h->W, h->H, h->D, h->d_min, h->dmap[0], h->agg3);
+  if (disp_out)
+    k_final<<<dim3((h->W + 127) / 128, h->H, 1), 128, 0, s>>>(h->dmap[0], h->dmap[1], h->agg3, h->W, h->H, 0, h->H,
+                                                              h->d_min, h->d_max, disp_out);
+  if (disp_l) cudaMemcpyAsync(disp_l, h->dmap[0], npix * 4, cudaMemcpyDeviceToDevice, s);
+  if (disp_r) cudaMemcpyAsync(disp_r, h->dmap[1], npix * 4, cudaMemcpyDeviceToDevice, s);
   return cuda_check(cudaGetLastError(), "fbs_debug_select");
 }
 
@@ -429,10 +538,10 @@ extern "C" int fbs_debug_maps(fbs_ctx* h, const uint8_t* left, const uint8_t* ri
   if (!h || !left || !right || !disp_out) return fail(FBS_E_ARG, "fbs_debug_maps: NULL argument");
   cudaStream_t s = (cudaStream_t)stream;
   const size_t npix = (size_t)h->W * h->H;
-  int rc = run_rows(h, left, right, 0, h->H, disp_out, nullptr, nullptr, s);
+  int rc = run(h, left, right, 1, 0, h->H, disp_out, nullptr, nullptr, s);
   if (rc != FBS_OK) return rc;
-  if (disp_l) cudaMemcpyAsync(disp_l, h->dL, npix * 4, cudaMemcpyDeviceToDevice, s);
-  if (disp_r) cudaMemcpyAsync(disp_r, h->dR, npix * 4, cudaMemcpyDeviceToDevice, s);
+  if (disp_l) cudaMemcpyAsync(disp_l, h->dmap[0], npix * 4, cudaMemcpyDeviceToDevice, s);
+  if (disp_r) cudaMemcpyAsync(disp_r, h->dmap[1], npix * 4, cudaMemcpyDeviceToDevice, s);
   return cuda_check(cudaGetLastError(), "fbs_debug_maps");
 }
 

@@ -53,14 +53,15 @@ def sass_of(function: str) -> str:
     raise AssertionError(f"{function} not in the SASS of libfbs.so")
 
 
-def test_sass_uses_ffma2():
-    """The aggregation inner loop issues FFMA2 with a broadcast scalar weight
-    (the radius-4 variant: 9 taps x 4 pixels per weight row)."""
-    out = sass_of("_ZN3fbs5k_aggILi4ELb0ELb0EEEvNS_7AggArgsE")
-    assert out.count("FFMA2") >= 24 * 81  # 4x6 px x 81 taps: the FMA stream is fully unrolled
+def test_sass_uses_ffma2_tma_dp4a():
+    """The fused kernel (radius 4): the aggregation stream issues FFMA2 with a
+    broadcast scalar weight (fully unrolled: 4x6 px x 81 taps per warp), the
+    cost rows are staged by TMA (UTMALDG) and the 3x3 dot products use DP4A."""
+    out = sass_of("_ZN3fbs5k_fbsILi4ELb0EEEvNS_8WalkArgsE")
+    assert out.count("FFMA2") >= 24 * 81
     assert re.search(r"FFMA2 R\d+, R\d+\.F32, R\d+\.F32x2", out)
-    cost = sass_of("_ZN3fbs6k_costENS_8CostArgsE")
-    assert "IDP.4A" in cost or "IDP4A" in cost
+    assert "UTMALDG" in out
+    assert "IDP.4A" in out or "IDP4A" in out
 
 
 @pytest.mark.parametrize("args,code", [

@@ -76,22 +76,13 @@ def test_volumes_and_maps(fbs, oracle_lib, case):
     # fbs_compute gives the same bytes as the debug path
     out2 = m.compute(Ld, Rd).cpu().numpy()
     assert np.array_equal(out2.view(np.uint32), out.view(np.uint32))
-    if name == "textureless":  # exercises every denominator form, with the EMPTY test on
-        import os
-        os.environ["FBS_EMPTY_FORM"] = "1"
-        try:
-            me = fbs.FBS(W, H, d_min, d_max, rho, gd, gr)
-        finally:
-            del os.environ["FBS_EMPTY_FORM"]
-        me.profile_enable(1)
-        out3 = me.compute(Ld, Rd).cpu().numpy()
-        forms = me.tile_stats()
-        me.profile_enable(0)
+    if name == "textureless":  # exercises every denominator form
+        m.profile_enable(1)
+        out3 = m.compute(Ld, Rd).cpu().numpy()
+        forms = m.tile_stats()
+        m.profile_enable(0)
         assert min(forms.values()) > 0, forms
         assert np.array_equal(out3.view(np.uint32), out.view(np.uint32))
-        _, _, al3, ar3 = (v.cpu().numpy() for v in me.volumes(Ld, Rd))
-        assert np.array_equal(al3.view(np.uint32), al.view(np.uint32))
-        assert np.array_equal(ar3.view(np.uint32), ar.view(np.uint32))
     # every disagreement was checked to be an oracle near-tie (gap < 1e-5); scenes
     # with textureless layers have many exact ties (perfect correlations at
     # several d), so the count is reported, not bounded
