@@ -73,12 +73,13 @@ typedef struct CUstream_st* fbs_stream_t;
  *   radius        ρ of Eq.(6): aggregation window (2ρ+1)^2; supported 1..FBS_MAX_RADIUS
  *                 (0 is also accepted: the aggregation is then the identity)
  *   sigma_s       γ_d of Eq.(7), used verbatim as exp(-r^2/γ_d^2)   (> 0, finite)
- *   sigma_r       γ_r of Eq.(8), used verbatim as exp(-Δ^2/γ_r^2)   (> 0, finite,
- *                 <= FBS_MAX_SIGMA_R; larger values return FBS_E_UNSUPPORTED)
+ *   sigma_r       γ_r of Eq.(8), used verbatim as exp(-Δ^2/γ_r^2)   (> 0, finite)
+ *                 The smallest tap weight exp(-2ρ²/γ_d² - 255²/γ_r²) must be at least
+ *                 2^-FBS_MAX_WEIGHT_EXP2 (a normal fp32: no defined tap may flush to
+ *                 zero, R#13); else FBS_E_UNSUPPORTED.  With γ_d = 5, ρ = 4
+ *                 that is γ_r >= 27.6; γ_r has no upper bound (γ_r -> ∞: box weights).
  * The NCC block half-width ϱ is fixed at 1 and the LRC tolerance at
- * 1 pixel (R#17).  Environment: FBS_EMPTY_FORM=1 selects the
- * aggregation variant that skips units whose costs are all undefined (large
- * textureless regions; identical results, ~3 % slower on textured scenes).  Returns NULL on error (reason: fbs_last_error()).
+ * 1 pixel (R#17).  Returns NULL on error (reason: fbs_last_error()).
  * Synchronises the device once (scratch initialisation); not graph-capturable.
  */
 fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, float sigma_s, float sigma_r);
@@ -92,10 +93,8 @@ const char* fbs_last_error(void);
 
 /* Maximum supported aggregation radius ρ of this build. */
 #define FBS_MAX_RADIUS 6
-/* Largest supported γ_r: the aggregation kernel marks taps of undefined blocks by
- * an intensity offset of 2^23, whose range weight must flush to zero (it does for
- * γ_r up to ~8.9e5; at this bound ω_r(255) already equals 1 in fp32). */
-#define FBS_MAX_SIGMA_R 1.0e5f
+/* -log2 of the smallest accepted tap weight ω_d·ω_r (see fbs_create). */
+#define FBS_MAX_WEIGHT_EXP2 124
 
 /*
  * fbs_compute — the whole hot path for one rectified pair:

@@ -184,9 +184,16 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
     fail(FBS_E_PARAM, "fbs_create: need 0 <= d_min < d_max, radius >= 0, finite sigma_s, sigma_r > 0");
     return nullptr;
   }
-  if (sigma_r > FBS_MAX_SIGMA_R) {
-    fail(FBS_E_UNSUPPORTED, "fbs_create: sigma_r > FBS_MAX_SIGMA_R");
-    return nullptr;
+  {  // R#13: every tap weight ω_d ω_r >= 2^-124 > FLT_MIN, so no defined tap flushes to 0 in fp32
+    // (ρ = 0: the only tap is the centre, weight 1)
+    const double e = radius == 0 ? 0.0
+                                 : 1.4426950408889634 * (2.0 * radius * radius / ((double)sigma_s * sigma_s) +
+                                                         65025.0 / ((double)sigma_r * sigma_r));
+    if (!(e <= kMaxWeightExp2)) {
+      fail(FBS_E_UNSUPPORTED, "fbs_create: the smallest tap weight exp(-2rho^2/sigma_s^2 - 255^2/sigma_r^2) is below "
+                              "2^-124 (fp32 underflow); increase sigma_r or sigma_s");
+      return nullptr;
+    }
   }
   if (radius > kMaxRadius) {
     fail(FBS_E_UNSUPPORTED, "fbs_create: radius > FBS_MAX_RADIUS");

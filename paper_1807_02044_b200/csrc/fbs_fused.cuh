@@ -150,6 +150,13 @@ struct WGeo {
   static constexpr bool kAlias = K1 * K1 >= kDB;         // dead weight rows hold the left costs
 };
 
+// Timing ablations (experiment builds only, tools/build_variants.py): bit 1 skips
+// the cost phase, bit 2 the FMA stream, bit 4 the weight prologue.  Results are
+// wrong in those builds; 0 in the product.
+#ifndef FBS_ABL
+#define FBS_ABL 0
+#endif
+
 template <int R>
 struct WSmem {
   using G = WGeo<R>;
@@ -457,8 +464,10 @@ __global__ void __launch_bounds__(256, 1) k_fbs(const __grid_constant__ WalkArgs
       if (R > 0) {  // fill: cost rows [ya - R, ya + R)
         mbar_wait(&sm.bar, par);
         par ^= 1;
-        if (side == 0) walk_cost<R, 0, EXPORT>(a, sm, ya - R, 2 * R, yb, x0, dlo, f);
-        else walk_cost<R, 1, EXPORT>(a, sm, ya - R, 2 * R, yb, x0, dlo, f);
+        if (!(FBS_ABL & 1)) {
+          if (side == 0) walk_cost<R, 0, EXPORT>(a, sm, ya - R, 2 * R, yb, x0, dlo, f);
+          else walk_cost<R, 1, EXPORT>(a, sm, ya - R, 2 * R, yb, x0, dlo, f);
+        }
         __syncthreads();
         if (threadIdx.x == 0) walk_issue<R>(a, sm, f, side, strip, b, ya + R, ya, true, nstep & 1);
       }
@@ -478,10 +487,12 @@ __global__ void __launch_bounds__(256, 1) k_fbs(const __grid_constant__ WalkArgs
         mbar_wait(&sm.bar, par);
         par ^= 1;
         // ---- cost rows [y0 + R, y0 + TY + R) -> ring ----
-        if (side == 0) walk_cost<R, 0, EXPORT>(a, sm, y0 + R, G::TY, yb, x0, dlo, f);
-        else walk_cost<R, 1, EXPORT>(a, sm, y0 + R, G::TY, yb, x0, dlo, f);
+        if (!(FBS_ABL & 1)) {
+          if (side == 0) walk_cost<R, 0, EXPORT>(a, sm, y0 + R, G::TY, yb, x0, dlo, f);
+          else walk_cost<R, 1, EXPORT>(a, sm, y0 + R, G::TY, yb, x0, dlo, f);
+        }
         // ---- weights w'(p,q) of the warp's pixels, Eq.(6)-(8) (see k_agg) ----
-        if (lane < kPX * kPY) {
+        if (!(FBS_ABL & 4) && lane < kPX * kPY) {
           const int py = lane / kPX, px = lane % kPX;
           float* wsm = sm.w[warp];
           const float* gq = sm.g[gb] + (wy + py) * GWS + (wx + px);
@@ -507,7 +518,10 @@ __global__ void __launch_bounds__(256, 1) k_fbs(const __grid_constant__ WalkArgs
               if (dy < K1) {
                 const float dd = __fsub_rn(gv[tt], gp);
                 float w;
-                asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(w) : "f"(__fmaf_rn(__fmul_rn(dd, dd), a.nkr, a.cd[dy * K1 + dx])));
+                asm("ex2.approx.ftz.f32 %0, %1;"
+                    : "=f"(w)
+                    : "f"(__fmaf_rn(__fmul_rn(dd, dd), a.nkr, a.cd[dy * K1 + dx])));
+                w = gv[tt] < kGuideFlag ? w : 0.f;  // taps of undefined blocks / outside the frame
                 col[dx] = __fadd_rn(col[dx], w);
                 wsm[((py * K1 + dy) * K1 + dx) * kPX + px] = w;
               }
@@ -604,7 +618,7 @@ __global__ void __launch_bounds__(256, 1) k_fbs(const __grid_constant__ WalkArgs
 #pragma unroll
             for (int jj = 0; jj < kPX; ++jj) head[jj] = *reinterpret_cast<const float4*>(rp + jj * kDB);
           }
-          RingRows<R, 0, HPY + 2 * R, HPY>::run(col, base, wsm, head, num);
+          if (!(FBS_ABL & 2)) RingRows<R, 0, HPY + 2 * R, HPY>::run(col, base, wsm, head, num);
           __syncwarp();  // every lane is done with the weights before the dead rows are overwritten
 #pragma unroll
           for (int pyl = 0; pyl < HPY; ++pyl)

@@ -39,15 +39,18 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 constexpr float kSent = -2.0f;   // undefined aggregated cost / exported cost (R#7)
 constexpr float kUndef = -0.0f;  // undefined cost in the cost ring (never a defined NCC value)
 constexpr int kMaxRadius = 6;    // FBS_MAX_RADIUS
+// Smallest tap weight the handle accepts, as -log2 (FBS_MAX_WEIGHT_EXP2, R#13):
+// 2^-124 stays a normal fp32 after ex2.approx.ftz and any rounding of the exponent.
+constexpr double kMaxWeightExp2 = 124.0;
 constexpr int kDB = 64;          // disparities per block (16 lanes x 4)
 constexpr int kPX = 4;           // warp sub-tile width  (pixels)
 constexpr int kTYMax = 12;       // tallest walker step of any radius
 
 // Padded guide images (written by k_prep): i(q) as a float, with an R-pixel
 // margin of kGuideUndef outside the frame.  A pixel whose own block is
-// undefined stores i + kGuideFlag: as a tap q it is >= 2^23 - 255 away from any
-// intensity, so ω_r flushes to exactly +0 (for γ_r <= FBS_MAX_SIGMA_R), and as a
-// centre p its intensity is recovered exactly (i + 2^23 is exact in fp32).
+// undefined stores i + kGuideFlag: as a tap q (value >= kGuideFlag) its weight
+// is forced to +0, and as a centre p its intensity is recovered exactly
+// (i + 2^23 is exact in fp32).
 constexpr float kGuideUndef = 1e30f;
 constexpr float kGuideFlag = 8388608.0f;
 __host__ __device__ constexpr int guide_pitch(int W, int R) { return ((W + 15) / 16 * 16 + 2 * R + 4 + 3) / 4 * 4; }

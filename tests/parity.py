@@ -1,16 +1,16 @@
 """GPU <-> oracle comparison rules (BASELINE.json north_star).
 
-  costs, aggregated costs   |gpu - ref| <= 1e-4 |ref| + ABS_FLOOR   (sentinel patterns equal)
+  costs, aggregated costs   |gpu - ref| <= 1e-6 |ref| + 1e-6         (sentinel patterns equal)
   integer WTA maps          bit-exact, except logged near-ties: allowed iff
                             agg_ref(p, d_gpu) >= agg_ref(p, d_ref) - 1e-5
   LRC mask                  exact where both maps (and the d_R they read) agree
   subpixel                  |gpu - ref| <= 1e-3 px where d and LRC agree; pixels whose
                             oracle parabola denominator |den| < 1e-3 are logged apart
 
-ABS_FLOOR is derived in DESIGN.md §4: an fp32 dot product of K <= 169 terms
-with normalised weights has forward error <= K u max|c| (u = 2^-24), i.e.
-<= 1.0e-5 for K = 169 and 4.8e-6 for K = 81; with |c| <= 1 we take
-ABS_FLOOR = K * 2^-24 + 1e-7 (cost: 1e-6).
+The aggregated-cost bound is SURVEY §8(c)'s 1e-6 (plus 1e-6 relative).  The
+rigorous fp32 worst case of a K-term weighted mean is ~2 K u (u = 2^-24:
+2.0e-5 at K = 169); the observed maximum over every GPU parity case is
+9.1e-7 (DESIGN.md §4 lists them per case), so the tight bound is the contract.
 """
 from __future__ import annotations
 
@@ -19,15 +19,15 @@ from dataclasses import dataclass, field
 import numpy as np
 
 SENT = -2.0
-REL = 1e-4
+REL = 1e-6
 TIE = 1e-5
 SUBPIX = 1e-3
 SMALL_DEN = 1e-3
 
 
 def agg_abs_floor(radius: int) -> float:
-    K = (2 * radius + 1) ** 2
-    return K * 2.0 ** -24 + 1e-7
+    """Absolute part of the aggregated-cost tolerance; radius-independent."""
+    return 1e-6
 
 
 def check_volume(gpu: np.ndarray, ref: np.ndarray, abs_floor: float, name: str):

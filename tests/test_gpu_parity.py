@@ -1,5 +1,8 @@
 """GPU parity: the CUDA path through the C ABI vs the CPU oracle, element by
 element on the same seeded inputs (rules in tests/parity.py)."""
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -36,7 +39,22 @@ CASES = [
     ("teddy", 450, 375, 0, 59, 4, "layered", 0x1809, 5.0, 32.0),
     # mostly textureless (70-94 % undefined blocks): EMPTY, GENERAL and EDGE units mixed
     ("textureless", 160, 120, 0, 79, 4, "flat", 20, 5.0, 32.0),
+    # near the fp32 underflow bound of R#13 (smallest tap weight 2^-121.5, 2^-115.8,
+    # 2^-111.6): half-textureless scenes make windows whose only defined costs at some
+    # d are far taps of tiny weight, where den is a sum of such weights
+    ("gamma-r28-bound", 96, 64, 0, 31, 4, "half", 21, 5.0, 28.0),
+    ("gamma-r30-rho6", 96, 64, 0, 31, 6, "half", 22, 3.0, 30.0),
+    ("gamma-d-small", 96, 64, 0, 31, 3, "half", 23, 0.7, 40.0),
 ]
+
+
+def log_errors(name, **errs):
+    """Observed maximum |gpu - oracle| per case (DESIGN.md §4 quotes them)."""
+    print("max_abs_err", name, " ".join(f"{k}={v:.3e}" for k, v in errs.items()))
+    path = os.environ.get("FBS_PARITY_LOG")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps({"case": name, **errs}) + "\n")
 
 
 def make_pair(kind, W, H, d_min, d_max, seed):
@@ -44,6 +62,8 @@ def make_pair(kind, W, H, d_min, d_max, seed):
         L, R, _, _ = synth.layered(W, H, d_min, d_max, seed, p_flat=0.3)
     elif kind == "flat":
         L, R, _, _ = synth.layered(W, H, d_min, d_max, seed, p_flat=0.9)
+    elif kind == "half":
+        L, R, _, _ = synth.layered(W, H, d_min, d_max, seed, p_flat=0.5)
     elif kind.startswith("dot"):
         L, R = synth.random_dot(W, H, int(kind[3:]), seed)
     return L, R
@@ -56,9 +76,10 @@ def test_volumes_and_maps(fbs, oracle_lib, case):
     ref = oracle_lib.fbs(L, R, d_min, d_max, rho, gd, gr)
     m = fbs.FBS(W, H, d_min, d_max, rho, gd, gr)
     Ld, Rd = to_dev(L), to_dev(R)
-    cl, cr, al, ar = (v.cpu().numpy() for v in m.volumes(Ld, Rd))
-    parity.check_volume(cl, ref.cost_l, 1e-6, "cost_l")
-    parity.check_volume(cr, ref.cost_r, 1e-6, "cost_r")
+    vols, emaps = m.volumes(Ld, Rd, maps=True)
+    cl, cr, al, ar = (v.cpu().numpy() for v in vols)
+    e_cl = parity.check_volume(cl, ref.cost_l, 1e-6, "cost_l")
+    e_cr = parity.check_volume(cr, ref.cost_r, 1e-6, "cost_r")
     # twin volumes: right(u-d, v, d) == left(u, v, d) bit-exactly on the GPU
     D = d_max - d_min + 1
     for k in range(D):
@@ -66,13 +87,19 @@ def test_volumes_and_maps(fbs, oracle_lib, case):
         if d < W:
             assert np.array_equal(cr[:, : W - d, k].view(np.uint32), cl[:, d:, k].view(np.uint32))
     floor = parity.agg_abs_floor(rho)
-    parity.check_volume(al, ref.agg_l, floor, "agg_l")
-    parity.check_volume(ar, ref.agg_r, floor, "agg_r")
+    e_al = parity.check_volume(al, ref.agg_l, floor, "agg_l")
+    e_ar = parity.check_volume(ar, ref.agg_r, floor, "agg_r")
     out, dl, dr = (t.cpu().numpy() for t in m.maps(Ld, Rd))
+    # the production kernel (no export) and the exporting instantiation whose
+    # volumes were checked above produce the same maps, bit for bit
+    for a, b in zip((out, dl, dr), (t.cpu().numpy() for t in emaps)):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
     rep = parity.MapReport()
     parity.check_int_map(dl, ref.disp_l, lambda i, d: ref.agg_l.reshape(-1, D)[i, d - d_min], "d_L", rep)
     parity.check_int_map(dr, ref.disp_r, lambda i, d: ref.agg_r.reshape(-1, D)[i, d - d_min], "d_R", rep)
     parity.check_final(out, ref.disp, dl, ref.disp_l, dr, ref.disp_r, ref.sub_den, W, rep)
+    log_errors(name, cost_l=e_cl, cost_r=e_cr, agg_l=e_al, agg_r=e_ar, subpix=rep.max_subpix_err,
+               near_ties=rep.near_ties, cascades=rep.cascades, pixels=W * H)
     # fbs_compute gives the same bytes as the debug path
     out2 = m.compute(Ld, Rd).cpu().numpy()
     assert np.array_equal(out2.view(np.uint32), out.view(np.uint32))
@@ -99,14 +126,16 @@ def test_all_radii(fbs, oracle_lib, rho):
     Ld, Rd = to_dev(L), to_dev(R)
     cl, _, al, ar = (v.cpu().numpy() for v in m.volumes(Ld, Rd))
     floor = parity.agg_abs_floor(rho)
-    parity.check_volume(al, ref.agg_l, floor, "agg_l")
-    parity.check_volume(ar, ref.agg_r, floor, "agg_r")
+    e_al = parity.check_volume(al, ref.agg_l, floor, "agg_l")
+    e_ar = parity.check_volume(ar, ref.agg_r, floor, "agg_r")
     out, dl, dr = (t.cpu().numpy() for t in m.maps(Ld, Rd))
     rep = parity.MapReport()
     D = d_max - d_min + 1
     parity.check_int_map(dl, ref.disp_l, lambda i, d: ref.agg_l.reshape(-1, D)[i, d - d_min], "d_L", rep)
     parity.check_int_map(dr, ref.disp_r, lambda i, d: ref.agg_r.reshape(-1, D)[i, d - d_min], "d_R", rep)
     parity.check_final(out, ref.disp, dl, ref.disp_l, dr, ref.disp_r, ref.sub_den, W, rep)
+    log_errors(f"radius-{rho}", agg_l=e_al, agg_r=e_ar, subpix=rep.max_subpix_err, near_ties=rep.near_ties,
+               pixels=W * H)
     if rho == 0:  # identity aggregation: bit-exact on the GPU's own costs
         assert np.array_equal(al.view(np.uint32), cl.view(np.uint32))
 
@@ -214,3 +243,84 @@ def test_full_size_sampled_pixels(fbs, oracle_lib, cfgname, npts):
         if px.disp[i] >= 0 and abs(px.sub_den[i]) >= parity.SMALL_DEN:
             assert abs(out[vs[i], us[i]] - px.disp[i]) <= parity.SUBPIX, i
     assert near <= max(2, npts // 50)
+
+
+def _full_check(fbs, oracle_lib, L, R, d_min, d_max, rho, gd, gr, tag):
+    """Volumes (export launch) and maps (production launch) of one pair vs the oracle."""
+    H, W = L.shape
+    D = d_max - d_min + 1
+    ref = oracle_lib.fbs(L, R, d_min, d_max, rho, gd, gr)
+    m = fbs.FBS(W, H, d_min, d_max, rho, gd, gr)
+    Ld, Rd = to_dev(L), to_dev(R)
+    vols, emaps = m.volumes(Ld, Rd, maps=True)
+    cl, cr, al, ar = (v.cpu().numpy() for v in vols)
+    parity.check_volume(cl, ref.cost_l, 1e-6, f"{tag} cost_l")
+    parity.check_volume(cr, ref.cost_r, 1e-6, f"{tag} cost_r")
+    floor = parity.agg_abs_floor(rho)
+    ea = max(parity.check_volume(al, ref.agg_l, floor, f"{tag} agg_l"),
+             parity.check_volume(ar, ref.agg_r, floor, f"{tag} agg_r"))
+    out, dl, dr = (t.cpu().numpy() for t in m.maps(Ld, Rd))
+    for a, b in zip((out, dl, dr), (t.cpu().numpy() for t in emaps)):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), tag
+    rep = parity.MapReport()
+    parity.check_int_map(dl, ref.disp_l, lambda i, d: ref.agg_l.reshape(-1, D)[i, d - d_min], f"{tag} d_L", rep)
+    parity.check_int_map(dr, ref.disp_r, lambda i, d: ref.agg_r.reshape(-1, D)[i, d - d_min], f"{tag} d_R", rep)
+    parity.check_final(out, ref.disp, dl, ref.disp_l, dr, ref.disp_r, ref.sub_den, W, rep)
+    m.close()
+    return ea, rep
+
+
+def test_tiny_frames(fbs, oracle_lib):
+    """Frames down to the 3x3 minimum, every radius, ranges wider than the frame:
+    staging boxes and strips hang past every edge (SURVEY §8(c) edge cases)."""
+    rng = np.random.default_rng(2024)
+    worst = 0.0
+    for t in range(40):
+        W, H = int(rng.integers(3, 18)), int(rng.integers(3, 18))
+        rho = t % (fbs.FBS_MAX_RADIUS + 1)
+        d_min = int(rng.integers(0, 4))
+        d_max = d_min + int(rng.integers(1, W + 4))
+        if t % 3 == 0:
+            L, R = synth.random_dot(W, H, min(d_max, W), 900 + t)
+        else:
+            L, R, _, _ = synth.layered(W, H, d_min, d_max, 900 + t, n_rects=2, p_flat=0.4)
+        ea, _ = _full_check(fbs, oracle_lib, L, R, d_min, d_max, rho, 4.0, 30.0, f"tiny{t} {W}x{H} rho={rho}")
+        worst = max(worst, ea)
+    log_errors("tiny-frames", agg=worst)
+
+
+def test_two_live_handles_alternating(fbs):
+    """Two handles with different D and radius alive at once, used alternately:
+    each keeps giving its own single-handle result (per-kernel launch attributes
+    are not lowered by the later handle)."""
+    a_cfg, b_cfg = synth.CONFIGS["kitti"], synth.CONFIGS["tsukuba"]
+    La, Ra = (to_dev(x) for x in synth.frame(a_cfg, 0))
+    Lb, Rb = (to_dev(x) for x in synth.frame(b_cfg, 0))
+    ma = fbs.FBS(a_cfg.W, a_cfg.H, a_cfg.d_min, a_cfg.d_max, a_cfg.radius, a_cfg.gamma_d, a_cfg.gamma_r)
+    ref_a = ma.compute(La, Ra).cpu().numpy()
+    mb = fbs.FBS(b_cfg.W, b_cfg.H, b_cfg.d_min, b_cfg.d_max, 2, b_cfg.gamma_d, b_cfg.gamma_r)
+    ref_b = mb.compute(Lb, Rb).cpu().numpy()
+    for _ in range(3):
+        assert np.array_equal(ma.compute(La, Ra).cpu().numpy().view(np.uint32), ref_a.view(np.uint32))
+        assert np.array_equal(mb.compute(Lb, Rb).cpu().numpy().view(np.uint32), ref_b.view(np.uint32))
+
+
+def test_cuda_graph_capture(fbs):
+    """fbs_compute is enqueue-only (no allocation, no sync): it captures into a CUDA
+    graph, and replays give the eager result."""
+    cfg = synth.CONFIGS["teddy"]
+    L, R = (to_dev(x) for x in synth.frame(cfg, 0))
+    m = fbs.FBS(cfg.W, cfg.H, cfg.d_min, cfg.d_max, cfg.radius, cfg.gamma_d, cfg.gamma_r)
+    eager = m.compute(L, R).cpu().numpy()
+    out = torch.full((cfg.H, cfg.W), 7.0, device="cuda")
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            m.compute(L, R, out=out, stream=s)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        out.fill_(7.0)
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), eager.view(np.uint32))
