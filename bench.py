@@ -142,10 +142,12 @@ def load_peak_fp32():
     return 148 * NOMINAL_FP32_LANES_PER_SM * 2 * mhz * 1e6 / 1e12, src
 
 
-def load_traffic(cfgname):
+def load_traffic(cfgname, path):
+    """dram read+write bytes of one launch of the dominant kernel, from the committed
+    ncu --set full summary (profiles/ncu_summary.json), else None."""
     try:
         s = json.load(open(PROFILE_SUMMARY))
-        return s.get(cfgname, {}).get("agg_dram_bytes_per_launch")
+        return s.get(f"{cfgname}/{path}", {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -164,7 +166,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     frames_np = [synth.frame(cfg, i + (0 if banded else 1000 * rank)) for i in range(nfr)]
     Ls = [torch.from_numpy(L).to(dev) for L, _ in frames_np]
     Rs = [torch.from_numpy(R).to(dev) for _, R in frames_np]
-    m = fbs.FBS(cfg.W, cfg.H, cfg.d_min, cfg.d_max, cfg.radius, cfg.gamma_d, cfg.gamma_r)
+    m = fbs.FBS(cfg.W, cfg.H, cfg.d_min, cfg.d_max, cfg.radius, cfg.gamma_d, cfg.gamma_r, path=args.path)
     out = torch.empty((cfg.H, cfg.W), dtype=torch.float32, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
@@ -253,7 +255,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         return None
     # ---- roofline of the dominant kernel (aggregation + WTA, both sides in one launch) ----
     peak, peak_src = load_peak_fp32()
-    agg_ms = stage_ms["fbs"] / max(1, nprof)
+    agg_ms = stage_ms["main"] / max(1, nprof)
     if banded:
         rows = fdist.band_range(cfg.H, rank, world)
         frac_rows = (rows[1] - rows[0]) / cfg.H
@@ -262,13 +264,17 @@ def run_ours(args, cfg, rank, world, local_rank):
     achieved = 2 * useful_flops_per_side(cfg) * frac_rows / (agg_ms * 1e-3) / 1e12
     tot_stage = sum(stage_ms.values())
     roof = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
-            "frac": round(achieved / peak, 4), "traffic": load_traffic(cfg.name),
-            "kernel": "k_agg (bilateral aggregation + WTA, both sides per launch)",
+            "frac": round(achieved / peak, 4), "traffic": load_traffic(cfg.name, args.path),
+            "kernel": ("k_agg (bilateral aggregation + WTA, both sides per launch; costs read from the "
+                       "L2/HBM volumes k_cost wrote)" if args.path == "volume" else
+                       "k_fbs_ws (fused: NCC costs into a shared-memory ring + aggregation + WTA, both sides)"),
             "avg_launch_ms": round(agg_ms, 5),
-            "timing": "k_agg launch duration from CUDA events on the launching stream around each "
+            "timing": "dominant-kernel launch duration from CUDA events on the launching stream around each "
                       "launch, in a profiled pass of the same workload right after the timed steps",
-            "share_of_step": round(stage_ms["fbs"] / tot_stage, 3) if tot_stage else None,
-            "stage_ms_per_frame": {k: round(v / max(1, nprof), 5) for k, v in stage_ms.items()},
+            "share_of_step": round(stage_ms["main"] / tot_stage, 3) if tot_stage else None,
+            "stage_ms_per_frame": {(("cost", "agg", "finalize") if args.path == "volume" else
+                                    ("prep", "fbs", "final"))[i]: round(v / max(1, nprof), 5)
+                                   for i, v in enumerate(stage_ms.values())},
             "peak_source": f"148 SM x 128 FP32 lanes x 2 x {peak_src} (nominal); "
                            "FFMA2 microbenchmark 66.9 TFLOP/s (DESIGN.md §6)",
             "useful_work": "numerator FMAs of Eq.(6): 2 sides x W*H*D*(2rho+1)^2 per launch",
@@ -359,6 +365,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="teddy", choices=sorted(synth.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--path", default="volume", choices=["volume", "fused"],
+                    help="implementation path (fbs_create_ex): volume (default, fastest) or fused")
     ap.add_argument("--e2e-batch", type=int, default=8,
                     help="frames per end-to-end step (fbs_compute_host_batch pipeline depth)")
     ap.add_argument("--radius", type=int, default=None,

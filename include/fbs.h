@@ -84,6 +84,22 @@ typedef struct CUstream_st* fbs_stream_t;
  */
 fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, float sigma_s, float sigma_r);
 
+/* Implementation paths (fbs_create_ex).  Both compute the same function, parity-
+ * tested against the same oracle:
+ *   FBS_PATH_VOLUME  (fbs_create's default) block statistics + twin cost volumes in
+ *                    device memory (L2-resident for Middlebury-sized frames), then
+ *                    aggregation + WTA reading them, then LRC + subpixel.  Fastest.
+ *   FBS_PATH_FUSED   costs computed into a shared-memory ring and aggregated there
+ *                    (never written to HBM); several frames per launch.  ~20x less
+ *                    DRAM traffic, ~20 % slower on B200 (profiles/ and DESIGN.md). */
+#define FBS_PATH_VOLUME 0
+#define FBS_PATH_FUSED 1
+
+/* fbs_create_ex — fbs_create with an explicit implementation path (above); an
+ * unknown path returns NULL (FBS_E_PARAM). */
+fbs_ctx* fbs_create_ex(int W, int H, int d_min, int d_max, int radius, float sigma_s, float sigma_r,
+                       int path);
+
 /* fbs_destroy — free the handle and its scratch.  The caller must have
  * synchronised all work enqueued with it.  NULL is a no-op. */
 void fbs_destroy(fbs_ctx* h);

@@ -22,13 +22,15 @@ FBS_E_ARG, FBS_E_PARAM, FBS_E_DIM, FBS_E_UNSUPPORTED, FBS_E_CUDA, FBS_E_OOM = -1
 FBS_INVALID = -1.0
 FBS_SENTINEL = -2.0
 FBS_MAX_RADIUS = 6
+FBS_PATH_VOLUME, FBS_PATH_FUSED = 0, 1
+PATHS = {"volume": FBS_PATH_VOLUME, "fused": FBS_PATH_FUSED}
 
 # every symbol include/fbs.h declares
-EXPORTS = ("fbs_create", "fbs_destroy", "fbs_last_error", "fbs_compute", "fbs_compute_rows",
+EXPORTS = ("fbs_create", "fbs_create_ex", "fbs_destroy", "fbs_last_error", "fbs_compute", "fbs_compute_rows",
            "fbs_compute_batch", "fbs_compute_host", "fbs_compute_host_batch", "fbs_debug_volumes", "fbs_debug_select",
            "fbs_debug_maps", "fbs_stats", "fbs_profile_enable", "fbs_profile_read", "fbs_tile_stats")
 FBS_NSTAGES = 3
-STAGES = ("prep", "fbs", "finalize")
+STAGES = ("prep", "main", "finalize")  # volume path: k_cost, k_agg, k_finalize; fused: k_prep, k_fbs, k_final
 
 _lib = None
 
@@ -50,6 +52,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     P, I, F = ctypes.c_void_p, ctypes.c_int, ctypes.c_float
     lib.fbs_create.argtypes = [I, I, I, I, I, F, F]
     lib.fbs_create.restype = P
+    lib.fbs_create_ex.argtypes = [I, I, I, I, I, F, F, I]
+    lib.fbs_create_ex.restype = P
     lib.fbs_destroy.argtypes = [P]
     lib.fbs_destroy.restype = None
     lib.fbs_last_error.argtypes = []
@@ -101,6 +105,14 @@ def _stream(stream):
 
 def fbs_create(W: int, H: int, d_min: int, d_max: int, radius: int, sigma_s: float, sigma_r: float):
     h = load_library().fbs_create(W, H, d_min, d_max, radius, sigma_s, sigma_r)
+    if not h:
+        raise FbsError(FBS_E_PARAM, last_error())
+    return ctypes.c_void_p(h)
+
+
+def fbs_create_ex(W: int, H: int, d_min: int, d_max: int, radius: int, sigma_s: float, sigma_r: float,
+                  path: int):
+    h = load_library().fbs_create_ex(W, H, d_min, d_max, radius, sigma_s, sigma_r, path)
     if not h:
         raise FbsError(FBS_E_PARAM, last_error())
     return ctypes.c_void_p(h)
@@ -184,7 +196,7 @@ class FBS:
     on the handle's device: uint8 [H, W] pairs in, float32 [H, W] map out."""
 
     def __init__(self, W: int, H: int, d_min: int, d_max: int, radius: int, sigma_s: float,
-                 sigma_r: float, device=None):
+                 sigma_r: float, device=None, path: str = "volume"):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_1807_02044_b200 needs a CUDA device (sm_100a); no CPU fallback")
@@ -192,8 +204,11 @@ class FBS:
         self.W, self.H, self.d_min, self.d_max, self.radius = W, H, d_min, d_max, radius
         self.sigma_s, self.sigma_r = sigma_s, sigma_r
         self.D = d_max - d_min + 1
+        if path not in PATHS:
+            raise ValueError(f"path must be one of {sorted(PATHS)}")
+        self.path = path
         with torch.cuda.device(self.device):
-            self.h = fbs_create(W, H, d_min, d_max, radius, sigma_s, sigma_r)
+            self.h = fbs_create_ex(W, H, d_min, d_max, radius, sigma_s, sigma_r, PATHS[path])
 
     def close(self):
         if getattr(self, "h", None):

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = [os.path.join(HERE, "csrc", "fbs_capi.cu")]
-DEPS = SRC + [os.path.join(HERE, "csrc", "fbs_kernels.cuh"), os.path.join(HERE, "csrc", "fbs_fused.cuh"), os.path.join(ROOT, "include", "fbs.h")]
+DEPS = SRC + [os.path.join(HERE, "csrc", "fbs_kernels.cuh"), os.path.join(HERE, "csrc", "fbs_fused.cuh"), os.path.join(HERE, "csrc", "fbs_ws.cuh"), os.path.join(HERE, "csrc", "fbs_volume.cuh"), os.path.join(ROOT, "include", "fbs.h")]
 OUT = os.path.join(HERE, "libfbs.so")
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

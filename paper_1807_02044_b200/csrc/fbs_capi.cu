@@ -2,8 +2,12 @@
 //
 // Host side: parameter validation, the ω_d / ω_r exponent constants (Eq.(7)(8),
 // built in double and rounded once to fp32, "pre-calculated"), scratch
-// allocation, TMA descriptors, and the launch sequence per batch of frames
-// (3 launches, programmatic dependent launch between them):
+// allocation, TMA descriptors, and the launch sequence.  Two paths compute the
+// same function:
+//   FBS_PATH_VOLUME (default, fbs_volume.cuh): k_cost -> L2/HBM cost volumes ->
+//                    k_agg -> k_finalize, one frame per launch sequence;
+//   FBS_PATH_FUSED (fbs_fused.cuh, fbs_ws.cuh): 3 launches per batch of frames,
+//                    programmatic dependent launch between them:
 //   k_prep   block statistics, packed columns, guides, masks   Eq.(2)(3)
 //   k_fbs    twin NCC costs in shared memory + aggregation    Eq.(1); Eq.(6)-(8)
 //            + WTA, both sides, all frames of the batch
@@ -14,17 +18,20 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <type_traits>
 #include <utility>
 
 #include <cuda.h>
 
 #include "../../include/fbs.h"
-#include "fbs_fused.cuh"
+#include "fbs_ws.cuh"
+#include "fbs_volume.cuh"
 
 using namespace fbs;
 
 struct fbs_ctx {
   WalkArgs wa;  // tensor maps, geometry and the Eq.(7)(8) constants (first: 64-B aligned)
+  int path;     // FBS_PATH_VOLUME / FBS_PATH_FUSED
   int W, H, d_min, d_max, D, nblk, R;
   float sigma_s, sigma_r;
   int device, num_sms;
@@ -39,6 +46,11 @@ struct fbs_ctx {
   int32_t* dmap[2];
   float4* agg3;
   unsigned long long* keys;
+  // volume path scratch (fbs_volume.cuh): padded cost volumes [Hv][nblk][Wv][64] per side,
+  // padded guides, block-defined masks, the left aggregated volume (multi-block frames)
+  int Wv, Hv, vWb, vWg;
+  float *volL, *volR, *gpadL, *gpadR, *aggL;
+  uint32_t *vbitsL, *vbitsR;
   // host path (fbs_compute_host[_batch]): two frame slots each, created on first use
   bool staging_ready;
   uint8_t *hL, *hR;
@@ -46,6 +58,7 @@ struct fbs_ctx {
   cudaStream_t cs_in, cs_out;
   cudaEvent_t ev_entry, ev_in[2], ev_done[2], ev_out[2];
   unsigned long long* tile_stats;  // device [4] FAST/EDGE/GENERAL/EMPTY, counting while profiling
+  unsigned long long* trace;       // FBS_TRACE builds: kernel timeline of CTA 0
   int launches;
   cudaEvent_t* prof_ev;  // live profiling (fbs_profile_enable): kEv events per call
   int prof_cap, prof_n;
@@ -66,17 +79,21 @@ static int cuda_check(cudaError_t e, const char* what) {
 extern "C" const char* fbs_last_error(void) { return g_err.c_str(); }
 
 // ---------------------------------------------------------------------------
-// Geometry per radius (the walker's compile-time traits)
+// Geometry per radius (the walker's compile-time traits): ρ <= 4 runs the
+// warp-specialised walker (SGeo, fbs_ws.cuh), ρ = 5, 6 the synchronous one (WGeo).
 template <int R>
-static void geo_of(int& TX, int& TY, size_t& smem) {
-  TX = WGeo<R>::TX;
-  TY = WGeo<R>::TY;
-  smem = sizeof(WSmem<R>) + 128;  // + alignment slack of the dynamic base
+using Geo = typename std::conditional<(R <= kWsMaxRadius), SGeo<R>, WGeo<R>>::type;
+template <int R>
+static void geo_of(int& TX, int& TY, size_t& smem, int& threads) {
+  TX = Geo<R>::TX;
+  TY = Geo<R>::TY;
+  threads = Geo<R>::THREADS;
+  smem = (R <= kWsMaxRadius ? sizeof(SSmem<R <= kWsMaxRadius ? R : 0>) : sizeof(WSmem<R>)) + 128;  // + alignment slack
 }
-static void geometry(int R, int& TX, int& TY, size_t& smem) {
+static void geometry(int R, int& TX, int& TY, size_t& smem, int& threads) {
   switch (R) {
 #define FBS_GEO(RR) \
-  case RR: geo_of<RR>(TX, TY, smem); break;
+  case RR: geo_of<RR>(TX, TY, smem, threads); break;
     FBS_GEO(0) FBS_GEO(1) FBS_GEO(2) FBS_GEO(3) FBS_GEO(4) FBS_GEO(5) FBS_GEO(6)
 #undef FBS_GEO
   }
@@ -115,7 +132,7 @@ static bool make_map(CUtensorMap* m, void* base, CUtensorMapDataType dt, int esi
 
 template <int R>
 static bool make_maps(fbs_ctx* h) {
-  using G = WGeo<R>;
+  using G = Geo<R>;
   bool ok = true;
   for (int im = 0; im < 2; ++im) {
     ok &= make_map(&h->wa.tmPs[im], h->P[im], CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, h->W, h->H, h->Wp, h->fcap, G::SPC,
@@ -162,7 +179,8 @@ static void free_host_path(fbs_ctx* h) {
 static void free_all(fbs_ctx* h) {
   free_host_path(h);
   void* ptrs[] = {h->P[0], h->P[1], h->SR[0], h->SR[1], h->G[0], h->G[1], h->bits[0], h->bits[1],
-                  h->dmap[0], h->dmap[1], h->agg3, h->keys, h->tile_stats};
+                  h->dmap[0], h->dmap[1], h->agg3, h->keys, h->tile_stats, h->trace,
+                  h->volL, h->volR, h->gpadL, h->gpadR, h->aggL, h->vbitsL, h->vbitsR};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -173,8 +191,19 @@ static size_t frame_bytes(const fbs_ctx* h) {
          npix * 16 + (h->nblk > 1 ? 2 * npix * 8 : 0);
 }
 
+static fbs_ctx* create_volume(fbs_ctx* h);
+
 extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, float sigma_s, float sigma_r) {
+  return fbs_create_ex(W, H, d_min, d_max, radius, sigma_s, sigma_r, FBS_PATH_VOLUME);
+}
+
+extern "C" fbs_ctx* fbs_create_ex(int W, int H, int d_min, int d_max, int radius, float sigma_s, float sigma_r,
+                                  int path) {
   g_err.clear();
+  if (path != FBS_PATH_VOLUME && path != FBS_PATH_FUSED) {
+    fail(FBS_E_PARAM, "fbs_create: path must be FBS_PATH_VOLUME or FBS_PATH_FUSED");
+    return nullptr;
+  }
   if (W < 3 || H < 3) {
     fail(FBS_E_DIM, "fbs_create: W and H must be >= 3 (one 3x3 NCC block)");
     return nullptr;
@@ -213,6 +242,7 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
     return nullptr;
   }
   std::memset((void*)h, 0, sizeof(*h));
+  h->path = path;
   h->W = W; h->H = H; h->d_min = d_min; h->d_max = d_max; h->D = d_max - d_min + 1;
   h->nblk = (h->D + kDB - 1) / kDB;
   h->R = radius;
@@ -220,7 +250,8 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
   cudaGetDevice(&h->device);
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
   size_t smem = 0;
-  geometry(radius, h->TX, h->TY, smem);
+  int threads = 0;
+  geometry(radius, h->TX, h->TY, smem, threads);
   h->Wp = (W + 3) / 4 * 4;
   h->Wg = guide_pitch(W, radius);
   h->GR = guide_rows(H, radius);
@@ -241,6 +272,7 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
     for (int dx = -radius; dx <= radius; ++dx)
       h->wa.cd[(dy + radius) * K1 + (dx + radius)] = (float)(-l2e * (double)(dx * dx + dy * dy) / (gd * gd));
   h->wa.nkr = (float)(-l2e / (gr * gr));
+  if (path == FBS_PATH_VOLUME) return create_volume(h);
 
   const size_t F = h->fcap, npix = (size_t)W * H;
   const size_t np = F * H * h->Wp;
@@ -255,6 +287,9 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
   ok &= cudaMalloc(&h->agg3, F * npix * sizeof(float4)) == cudaSuccess;
   if (h->nblk > 1) ok &= cudaMalloc(&h->keys, 2 * F * npix * 8) == cudaSuccess;
   ok &= cudaMalloc(&h->tile_stats, 4 * sizeof(unsigned long long)) == cudaSuccess;
+#ifdef FBS_TRACE
+  ok &= cudaMalloc(&h->trace, 8192 * sizeof(unsigned long long)) == cudaSuccess;
+#endif
   if (!ok) {
     cudaGetLastError();
     free_all(h);
@@ -281,14 +316,20 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
   }
   // fixed per instantiation, so setting it per handle never lowers another handle's cap
   switch (radius) {
+#define FBS_SMEM_WS(RR)                                                                                    \
+  case RR:                                                                                                 \
+    cudaFuncSetAttribute(k_fbs_ws<RR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+    cudaFuncSetAttribute(k_fbs_ws<RR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
+    break;
 #define FBS_SMEM_ATTR(RR)                                                                                  \
   case RR:                                                                                                 \
     cudaFuncSetAttribute(k_fbs<RR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
     cudaFuncSetAttribute(k_fbs<RR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
     break;
-    FBS_SMEM_ATTR(0) FBS_SMEM_ATTR(1) FBS_SMEM_ATTR(2) FBS_SMEM_ATTR(3) FBS_SMEM_ATTR(4) FBS_SMEM_ATTR(5)
+    FBS_SMEM_WS(0) FBS_SMEM_WS(1) FBS_SMEM_WS(2) FBS_SMEM_WS(3) FBS_SMEM_WS(4) FBS_SMEM_ATTR(5)
     FBS_SMEM_ATTR(6)
 #undef FBS_SMEM_ATTR
+#undef FBS_SMEM_WS
   }
   if (cuda_check(cudaGetLastError(), "fbs_create smem attributes") != FBS_OK) {
     free_all(h);
@@ -304,6 +345,76 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
   a.agg3 = h->agg3;
   a.keys = h->keys;
   a.nstrips = (W + h->TX - 1) / h->TX;
+  return h;
+}
+
+// Volume path scratch (one frame): FBS_PATH_VOLUME.
+static fbs_ctx* create_volume(fbs_ctx* h) {
+  const int W = h->W, H = h->H, R = h->R;
+  h->fcap = 1;
+  h->TX = vol::kTX;
+  h->TY = vol::agg_tile_h(R);
+  h->Wv = (W + vol::kTX - 1) / vol::kTX * vol::kTX + 2 * R;
+  h->Hv = (H + vol::kTYMax - 1) / vol::kTYMax * vol::kTYMax + vol::kTYMax + 2 * R;
+  h->vWb = (W + vol::kCX - 1) / vol::kCX * (vol::kCX / 32);
+  h->vWg = vol::guide_pitch(W, R);
+  const size_t npix = (size_t)W * H;
+  const size_t nvol = (size_t)h->Hv * h->Wv * h->nblk * kDB;
+  const size_t ngp = (size_t)vol::guide_rows(H, R) * h->vWg;
+  bool ok = true;
+  ok &= cudaMalloc(&h->gpadL, ngp * 4) == cudaSuccess;
+  ok &= cudaMalloc(&h->gpadR, ngp * 4) == cudaSuccess;
+  ok &= cudaMalloc(&h->vbitsL, (size_t)H * h->vWb * 4) == cudaSuccess;
+  ok &= cudaMalloc(&h->vbitsR, (size_t)H * h->vWb * 4) == cudaSuccess;
+  ok &= cudaMalloc(&h->volL, nvol * 4) == cudaSuccess;
+  ok &= cudaMalloc(&h->volR, nvol * 4) == cudaSuccess;
+  ok &= cudaMalloc(&h->dmap[0], npix * 4) == cudaSuccess;
+  ok &= cudaMalloc(&h->dmap[1], npix * 4) == cudaSuccess;
+  if (h->nblk > 1) ok &= cudaMalloc(&h->aggL, npix * h->nblk * kDB * sizeof(float)) == cudaSuccess;
+  ok &= cudaMalloc(&h->agg3, npix * sizeof(float4)) == cudaSuccess;
+  ok &= cudaMalloc(&h->tile_stats, 4 * sizeof(unsigned long long)) == cudaSuccess;
+#ifdef FBS_TRACE
+  ok &= cudaMalloc(&h->trace, 8192 * sizeof(unsigned long long)) == cudaSuccess;
+#endif
+  if (!ok) {
+    cudaGetLastError();
+    free_all(h);
+    delete h;
+    fail(FBS_E_OOM, "fbs_create: device allocation failed");
+    return nullptr;
+  }
+  // margins (and never-written rows) of the volumes hold the undefined cost
+  vol::k_fill<<<1184, 256>>>(h->volL, nvol, kUndef);
+  vol::k_fill<<<1184, 256>>>(h->volR, nvol, kUndef);
+  vol::k_fill<<<256, 256>>>(h->gpadL, ngp, kGuideUndef);  // margins: taps outside the frame
+  vol::k_fill<<<256, 256>>>(h->gpadR, ngp, kGuideUndef);
+  cudaMemset(h->tile_stats, 0, 4 * sizeof(unsigned long long));
+  cudaMemset(h->dmap[0], 0xff, npix * 4);
+  cudaMemset(h->dmap[1], 0xff, npix * 4);
+  cudaMemset(h->vbitsL, 0, (size_t)H * h->vWb * 4);
+  cudaMemset(h->vbitsR, 0, (size_t)H * h->vWb * 4);
+  if (cuda_check(cudaDeviceSynchronize(), "fbs_create init") != FBS_OK) {
+    free_all(h);
+    delete h;
+    return nullptr;
+  }
+  // fixed per instantiation (k_cost: the largest supported block count), so a later
+  // handle never lowers another handle's cap
+#define FBS_SMEM_ATTR(RR)                                                                                     \
+  cudaFuncSetAttribute(vol::k_agg<RR, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,             \
+                       sizeof(vol::AggSmem<RR>));                                                             \
+  cudaFuncSetAttribute(vol::k_agg<RR, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
+                       sizeof(vol::AggSmem<RR>));
+  FBS_SMEM_ATTR(0) FBS_SMEM_ATTR(1) FBS_SMEM_ATTR(2) FBS_SMEM_ATTR(3) FBS_SMEM_ATTR(4)
+  FBS_SMEM_ATTR(5) FBS_SMEM_ATTR(6)
+#undef FBS_SMEM_ATTR
+  cudaFuncSetAttribute(vol::k_cost, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)vol::cost_smem_bytes(4096 / kDB));
+  if (cuda_check(cudaGetLastError(), "fbs_create smem attributes") != FBS_OK) {
+    free_all(h);
+    delete h;
+    return nullptr;
+  }
   return h;
 }
 
@@ -344,24 +455,128 @@ static cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 
 static cudaError_t launch_walk(const fbs_ctx* h, const WalkArgs& a, bool exp, cudaStream_t s) {
   const long long g = a.total < h->num_sms ? a.total : h->num_sms;
-  int tx, ty;
+  int tx, ty, threads;
   size_t smem;
-  geometry(h->R, tx, ty, smem);
+  geometry(h->R, tx, ty, smem, threads);
+  const dim3 grid((unsigned)g), block((unsigned)threads);
   switch (h->R) {
-#define FBS_CASE(RR)                                                                                 \
-  case RR:                                                                                           \
-    return exp ? launch_pdl(k_fbs<RR, true>, dim3((unsigned)g), dim3(256), smem, s, a)               \
-               : launch_pdl(k_fbs<RR, false>, dim3((unsigned)g), dim3(256), smem, s, a);
-    FBS_CASE(0) FBS_CASE(1) FBS_CASE(2) FBS_CASE(3) FBS_CASE(4) FBS_CASE(5) FBS_CASE(6)
+#define FBS_CASE_WS(RR)                                                                                   \
+  case RR:                                                                                                \
+    return exp ? launch_pdl(k_fbs_ws<RR, true>, grid, block, smem, s, a)                                  \
+               : launch_pdl(k_fbs_ws<RR, false>, grid, block, smem, s, a);
+#define FBS_CASE(RR)                                                                                      \
+  case RR:                                                                                                \
+    return exp ? launch_pdl(k_fbs<RR, true>, grid, block, smem, s, a)                                     \
+               : launch_pdl(k_fbs<RR, false>, grid, block, smem, s, a);
+    FBS_CASE_WS(0) FBS_CASE_WS(1) FBS_CASE_WS(2) FBS_CASE_WS(3) FBS_CASE_WS(4) FBS_CASE(5) FBS_CASE(6)
 #undef FBS_CASE
+#undef FBS_CASE_WS
   }
   return cudaErrorInvalidValue;
+}
+
+// Volume path, one frame: output rows [r0, r1); exports when expC/expA are set.
+static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0, int r1, float* out,
+                      float* const* expC, float* const* expA, cudaStream_t s) {
+  const int W = h->W, H = h->H, R = h->R;
+  // aggregation tiles are anchored at multiples of the tile height in frame rows, so a
+  // pixel's denominator form never depends on the band; cost rows cover the
+  // tiles' windows (the classification reads validity masks over them too)
+  const int TY = vol::agg_tile_h(R);
+  const int ty0 = r0 / TY, ty1 = (r1 + TY - 1) / TY;
+  const int c0 = std::max(0, ty0 * TY - R), c1 = std::min(H, ty1 * TY + R);  // cost rows
+  float* aggL_exp = expA ? expA[0] : nullptr;
+  float* aggR_exp = expA ? expA[1] : nullptr;
+  h->launches = 0;
+  cudaEvent_t* ev = nullptr;
+  if (h->prof_ev && h->prof_n < h->prof_cap) ev = h->prof_ev + kEv * h->prof_n++;
+  if (ev) cudaEventRecord(ev[0], s);
+  {
+    vol::CostArgs ca;
+    ca.W = W; ca.H = H; ca.D = h->D; ca.d_min = h->d_min; ca.nblk = h->nblk; ca.Wv = h->Wv; ca.R = R;
+    ca.r0 = c0; ca.r1 = c1;
+    ca.L = L; ca.Rimg = Rimg; ca.volL = h->volL; ca.volR = h->volR;
+    ca.bitsL = h->vbitsL; ca.bitsR = h->vbitsR; ca.Wb = h->vWb;
+    ca.gpadL = h->gpadL; ca.gpadR = h->gpadR; ca.Wg = h->vWg;
+    const dim3 grd((W + vol::kCX - 1) / vol::kCX, c1 - c0, 2);
+    vol::k_cost<<<grd, 256, vol::cost_smem_bytes(h->nblk), s>>>(ca);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_check(e, "k_cost launch");  // nothing downstream runs on stale volumes
+    h->launches += 1;
+  }
+  if (ev) cudaEventRecord(ev[1], s);
+  vol::AggArgs a;
+  a.W = W; a.H = H; a.D = h->D; a.d_min = h->d_min; a.d_max = h->d_max;
+  a.nblk = h->nblk; a.Wv = h->Wv;
+  std::memcpy(a.cd, h->wa.cd, sizeof(a.cd));
+  a.nkr = h->wa.nkr;
+  a.gpadL = h->gpadL; a.gpadR = h->gpadR; a.Wg = h->vWg;
+  a.r0 = r0; a.r1 = r1; a.ty0 = ty0;
+  a.volL = h->volL; a.volR = h->volR;
+  a.bitsL = h->vbitsL; a.bitsR = h->vbitsR; a.Wb = h->vWb;
+  a.dL = h->dmap[0]; a.dR = h->dmap[1]; a.aggL = h->aggL; a.exportR = aggR_exp;
+  // one d-block: the left costs stay on chip and only Eq.(10)'s three are stored
+  // (unless the debug export wants the whole left volume)
+  float* aggL_tmp = nullptr;
+  if (aggL_exp && !h->aggL) {  // single-block frame exporting its left volume: temporary store
+    if (cudaMalloc(&aggL_tmp, (size_t)W * H * kDB * sizeof(float)) != cudaSuccess)
+      return fail(FBS_E_OOM, "fbs_debug_volumes: scratch");
+    a.aggL = aggL_tmp;
+  }
+  a.agg3 = (h->nblk == 1 && !aggL_exp) ? h->agg3 : nullptr;
+  a.tile_stats = ev ? h->tile_stats : nullptr;
+  {
+    const dim3 grid((W + vol::kTX - 1) / vol::kTX, ty1 - ty0, 2);
+    cudaError_t e = cudaErrorInvalidValue;
+    switch (R) {
+#define FBS_CASE(RR)                                                                                          \
+  case RR:                                                                                                    \
+    e = aggR_exp ? launch_pdl(vol::k_agg<RR, false, true>, grid, dim3(vol::AggGeom<RR>::THREADS),             \
+                              sizeof(vol::AggSmem<RR>), s, a)                                                 \
+                 : launch_pdl(vol::k_agg<RR, false, false>, grid, dim3(vol::AggGeom<RR>::THREADS),            \
+                              sizeof(vol::AggSmem<RR>), s, a);                                                \
+    break;
+      FBS_CASE(0) FBS_CASE(1) FBS_CASE(2) FBS_CASE(3) FBS_CASE(4) FBS_CASE(5) FBS_CASE(6)
+#undef FBS_CASE
+    }
+    if (e != cudaSuccess) return cuda_check(e, "k_agg launch");
+    h->launches += 1;
+  }
+  if (ev) cudaEventRecord(ev[2], s);
+  {
+    const dim3 grd((W + 127) / 128, r1 - r0);
+    const cudaError_t e = launch_pdl(vol::k_finalize, grd, dim3(128), 0, s, (const int32_t*)h->dmap[0],
+                                     (const int32_t*)h->dmap[1], (const float*)a.aggL, (const float4*)a.agg3,
+                                     h->nblk, W, r0, r1, h->d_min, h->d_max, out);
+    if (e != cudaSuccess) return cuda_check(e, "k_finalize launch");
+    h->launches += 1;
+  }
+  if (ev) cudaEventRecord(ev[3], s);
+  if (aggL_exp) vol::k_export_agg<<<1184, 256, 0, s>>>(a.aggL, W, H, h->D, h->nblk, aggL_exp);
+  if (expC && expC[0]) vol::k_export_vol<<<1184, 256, 0, s>>>(h->volL, W, H, h->D, h->nblk, h->Wv, R, expC[0]);
+  if (expC && expC[1]) vol::k_export_vol<<<1184, 256, 0, s>>>(h->volR, W, H, h->D, h->nblk, h->Wv, R, expC[1]);
+  if (aggL_tmp) {
+    cudaStreamSynchronize(s);
+    cudaFree(aggL_tmp);
+  }
+  return cuda_check(cudaGetLastError(), "fbs launch");
 }
 
 // nf frames (left/right: nf x [H][W] device), output rows [r0, r1) of each into
 // out (nf x [r1-r0][W]); exports (one frame) when expC/expA are set.
 static int run(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int nf, int r0, int r1, float* out,
                float* const* expC, float* const* expA, cudaStream_t s) {
+  if (h->path == FBS_PATH_VOLUME) {
+    const size_t npix = (size_t)h->W * h->H, nout = (size_t)(r1 - r0) * h->W;
+    int launches = 0;
+    for (int i = 0; i < nf; ++i) {
+      const int rc = run_volume(h, L + i * npix, Rimg + i * npix, r0, r1, out + i * nout, expC, expA, s);
+      if (rc != FBS_OK) return rc;
+      launches += h->launches;
+    }
+    h->launches = launches;
+    return FBS_OK;
+  }
   const int W = h->W, H = h->H, R = h->R, TY = h->TY;
   // walker steps are anchored at multiples of TY in frame rows, so a pixel's
   // denominator form never depends on the band; cost rows cover their windows
@@ -391,6 +606,7 @@ static int run(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int nf, int r0
     a.expC[0] = expC ? expC[0] : nullptr; a.expC[1] = expC ? expC[1] : nullptr;
     a.expA[0] = expA ? expA[0] : nullptr; a.expA[1] = expA ? expA[1] : nullptr;
     a.tile_stats = ev ? h->tile_stats : nullptr;
+    a.trace = h->trace;
     e = launch_walk(h, a, expC || expA, s);
     if (e != cudaSuccess) return cuda_check(e, "k_fbs launch");
     h->launches += 1;
@@ -606,3 +822,11 @@ extern "C" int fbs_tile_stats(fbs_ctx* h, long long* fast, long long* edge, long
   if (empty) *empty = (long long)v[3];
   return FBS_OK;
 }
+
+#ifdef FBS_TRACE
+// Trace builds only (not in include/fbs.h): copy the last launch's timeline of CTA 0.
+extern "C" int fbs_debug_trace(fbs_ctx* h, unsigned long long* host, int n) {
+  if (!h || !h->trace || !host || n > 8192) return fail(FBS_E_ARG, "fbs_debug_trace");
+  return cuda_check(cudaMemcpy(host, h->trace, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "trace");
+}
+#endif

@@ -97,12 +97,17 @@ __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned coun
 __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+#ifndef FBS_SUSPEND_HINT
+#define FBS_SUSPEND_HINT 0x989680
+#endif
+// try_wait with a suspend-time hint: the waiting warp sleeps in hardware until
+// the phase completes (or the hint expires) instead of spinning on issue slots.
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(FBS_SUSPEND_HINT)
       : "memory");
 }
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, unsigned long long* bar, int x, int y,
@@ -124,6 +129,7 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // x 64 disparities.  One CTA per SM (the ring + weights use ~220 KB).
 template <int R>
 struct WGeo {
+  static constexpr int RR = R;
   static constexpr int K1 = 2 * R + 1;
   static constexpr int HPY = R <= 4 ? 3 : (R == 5 ? 2 : 1);
   static constexpr int PY = 2 * HPY;
@@ -132,6 +138,7 @@ struct WGeo {
   static constexpr int TY = PY * NWY;
   static constexpr int SC = TX + 2 * R;  // ring columns: x0-R .. x0+TX+R-1
   static constexpr int SR = TY + 2 * R;  // ring rows
+  static constexpr int NSLOT = SR;       // ring slots (a frame row's slot: row index mod NSLOT)
   static constexpr int CU = SC / 2;      // positions per cost unit (half a ring row)
   // staging (TMA boxes; inner extent x element size a multiple of 16 B).  A box
   // must also START at a 16-B aligned x (measured on this part: other starts
@@ -151,7 +158,8 @@ struct WGeo {
 };
 
 // Timing ablations (experiment builds only, tools/build_variants.py): bit 1 skips
-// the cost phase, bit 2 the FMA stream, bit 4 the weight prologue.  Results are
+// the cost phase, bit 2 the FMA stream, bit 4 the weight prologue, bit 8 (k_fbs_ws)
+// the TMA loads.  Results are
 // wrong in those builds; 0 in the product.
 #ifndef FBS_ABL
 #define FBS_ABL 0
@@ -188,6 +196,7 @@ struct WalkArgs {
   float* expC[2];           // EXPORT: cost volumes [F=1][H][W][D], FBS_SENTINEL = undefined
   float* expA[2];           // EXPORT: aggregated volumes
   unsigned long long* tile_stats;
+  unsigned long long* trace;  // FBS_TRACE builds only: clock64 stamps of CTA 0 (else null)
   float nkr;
   float cd[(2 * kMaxRadius + 1) * (2 * kMaxRadius + 1)];
 };
@@ -209,12 +218,13 @@ struct WOff {
 // exact and conservative: EDGE if the frame edge cuts taps off, GENERAL if the
 // other image has an undefined block anywhere in the shifted range (<= 16 rows
 // x 4 mask words, two per lane).
-template <int R>
+template <class G>
 struct WCw {
   int qy0, lo, hi, edge, nw, rows, w0;
   __device__ __forceinline__ WCw(int W, int H, int d_min, int d_max, int side, int sx, int sy, int b) {
+    constexpr int R = G::RR;
     qy0 = max(sy - R, 1);
-    const int qy1 = min(sy + WGeo<R>::PY - 1 + R, H - 2);
+    const int qy1 = min(sy + G::PY - 1 + R, H - 2);
     const int qx0 = max(sx - R, 1), qx1 = min(sx + kPX - 1 + R, W - 2);
     const int d_lo = d_min + b * kDB, d_hi = min(d_lo + kDB - 1, d_max);
     if (side == 0) { lo = qx0 - d_hi; hi = qx1 - d_lo; edge = lo < 1; lo = max(lo, 1); }
@@ -237,24 +247,29 @@ struct WCw {
 // dot product is the sum of three DP4A column dots shared along the unit.
 // Both sides evaluate N · (r_self · r_other) with the same exact integer N and
 // a commutative product, so right(u-d,v,d) == left(u,v,d) bit-exactly.
-template <int R, int SIDE, bool EXPORT>
-__device__ __forceinline__ void walk_cost(const WalkArgs& a, WSmem<R>& sm, int yc, int n, int yb, int x0, int dlo,
-                                          int f) {
-  using G = WGeo<R>;
+// Geometry-generic form: staging buffers Ps/Po/Ss/So, ring [G::NSLOT][G::SC][64];
+// row yc + t goes to ring slot (slot0 + t) mod NSLOT; units (row, half) u =
+// u0, u0 + us, ... (the calling warps).
+template <class G, int SIDE, bool EXPORT>
+__device__ __forceinline__ void walk_cost_g(const WalkArgs& a, float (*ring)[G::SC][kDB], const uint32_t* Ps,
+                                            const uint32_t* Po, const int2* Ss, const int2* So, int yc, int n,
+                                            int slot0, int x0, int dlo, int u0, int us) {
+  constexpr int R = G::RR;
   constexpr int CU = G::CU;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int k0 = 2 * lane;
   const bool pad0 = dlo + k0 > a.d_max, pad1 = dlo + k0 + 1 > a.d_max;
   const WOff off(R, x0, SIDE, dlo);
-  for (int u = warp; u < 2 * n; u += G::NW) {
+  for (int u = u0; u < 2 * n; u += us) {
     const int yy = u >> 1, i0 = (u & 1) * CU;
     const int y = yc + yy;
-    int slot = (y - yb) % G::SR;
-    float* dst = &sm.ring[slot][i0][k0];
+    int slot = slot0 + yy;
+    if (slot >= G::NSLOT) slot -= G::NSLOT;
+    float* dst = &ring[slot][i0][k0];
     // self packed columns of positions i0-1 .. i0+CU (staging col ip = i + 1)
-    const uint32_t* ps = sm.Ps + yy * G::SPC + off.ps + i0;
+    const uint32_t* ps = Ps + yy * G::SPC + off.ps + i0;
     // other packed columns: side 0 jp = i - k + 64 (k0: i0-1+m - k0 + 64); side 1 jp = i + k + 1
-    const uint32_t* pob = sm.Po + yy * G::OPC + off.po + (SIDE == 0 ? i0 + 63 - k0 - 1 : i0 + k0);
+    const uint32_t* pob = Po + yy * G::OPC + off.po + (SIDE == 0 ? i0 + 63 - k0 - 1 : i0 + k0);
     uint32_t po[CU + 3];
 #pragma unroll
     for (int m = 0; m < CU + 3; ++m) po[m] = pob[m];
@@ -266,8 +281,8 @@ __device__ __forceinline__ void walk_cost(const WalkArgs& a, WSmem<R>& sm, int y
       cd1[m] = (int)__dp4a(s, SIDE == 0 ? po[m] : po[m + 1], 0u);
     }
     // statistics: self position i -> Ss[i]; other: side 0 j = i - k + 63, side 1 j = i + k
-    const int2* ss = sm.Ss + yy * G::SSC + off.ss + i0;
-    const int2* sob = sm.So + yy * G::OSC + off.so + (SIDE == 0 ? i0 + 63 - k0 - 1 : i0 + k0);
+    const int2* ss = Ss + yy * G::SSC + off.ss + i0;
+    const int2* sob = So + yy * G::OSC + off.so + (SIDE == 0 ? i0 + 63 - k0 - 1 : i0 + k0);
     int2 so[CU + 1];
 #pragma unroll
     for (int m = 0; m < CU + 1; ++m) so[m] = sob[m];
@@ -302,45 +317,137 @@ __device__ __forceinline__ void walk_cost(const WalkArgs& a, WSmem<R>& sm, int y
   }
 }
 
+template <int R, int SIDE, bool EXPORT>
+__device__ __forceinline__ void walk_cost(const WalkArgs& a, WSmem<R>& sm, int yc, int n, int yb, int x0, int dlo,
+                                          int f) {
+  using G = WGeo<R>;
+  walk_cost_g<G, SIDE, EXPORT>(a, sm.ring, sm.Ps, sm.Po, sm.Ss, sm.So, yc, n, (yc - yb) % G::SR, x0, dlo,
+                               threadIdx.x >> 5, G::NW);
+}
+
 // Numerator stream over the ring (FAST / EDGE): as Rows4 in k_agg, cost row r of
 // the half-warp lives in ring slot (base + r) mod SR.
-template <int R, int r, int NR, int NPY>
+template <class G, int r, int NR, int NPY>
 struct RingRows {
   static __device__ __forceinline__ void run(const float* __restrict__ col, int base, const float* __restrict__ wsm,
                                              float4 (&head)[kPX], float2 (&num)[NPY][kPX][2]) {
-    using G = WGeo<R>;
+    constexpr int R = G::RR;
     constexpr int NC = kPX + 2 * R;
     constexpr int RS = G::SC * kDB;
     float4 c[NC];
 #pragma unroll
     for (int j = 0; j < kPX; ++j) c[j] = head[j];
     int s = base + r;
-    if (s >= G::SR) s -= G::SR;
+    if (s >= G::NSLOT) s -= G::NSLOT;
     const float* rp = col + s * RS;
 #pragma unroll
     for (int j = kPX; j < NC; ++j) c[j] = *reinterpret_cast<const float4*>(rp + j * kDB);
     if constexpr (r + 1 < NR) {
       int s1 = s + 1;
-      if (s1 >= G::SR) s1 -= G::SR;
+      if (s1 >= G::NSLOT) s1 -= G::NSLOT;
       const float* rn = col + s1 * RS;
 #pragma unroll
       for (int j = 0; j < kPX; ++j) head[j] = *reinterpret_cast<const float4*>(rn + j * kDB);
     }
     row_fma4<R, NPY, r>(c, wsm, num);
-    RingRows<R, r + 1, NR, NPY>::run(col, base, wsm, head, num);
+    RingRows<G, r + 1, NR, NPY>::run(col, base, wsm, head, num);
   }
 };
-template <int R, int NR, int NPY>
-struct RingRows<R, NR, NR, NPY> {
+template <class G, int NR, int NPY>
+struct RingRows<G, NR, NR, NPY> {
   static __device__ __forceinline__ void run(const float*, int, const float*, float4 (&)[kPX],
                                              float2 (&)[NPY][kPX][2]) {}
 };
 
+// Compact form of the stream (the warp-specialised walker: producer and
+// consumer warps share the SM's instruction caches, so the stream must be
+// small).  Rows that feed only some of the NPY output rows (the first NPY-1
+// and the last NPY-1 cost rows) are unrolled at compile time; the cost rows
+// that feed all NPY output rows run in a loop whose body is one cost row
+// (NC LDS.128 + NPY*K1 weight LDS.128 + NPY*K1*8 FFMA2).  Per accumulator the
+// summation order is the same as RingRows (dy ascending, then dx).
+template <class G, int r, int NPY>
+__device__ __forceinline__ void ring_row_ct(const float* __restrict__ col, int base, const float* __restrict__ wsm,
+                                            float2 (&num)[NPY][kPX][2]) {
+  constexpr int R = G::RR;
+  constexpr int NC = kPX + 2 * R;
+  int s = base + r;
+  if (s >= G::NSLOT) s -= G::NSLOT;
+  const float* rp = col + s * (G::SC * kDB);
+  float4 c[NC];
+#pragma unroll
+  for (int j = 0; j < NC; ++j) c[j] = *reinterpret_cast<const float4*>(rp + j * kDB);
+  row_fma4<R, NPY, r>(c, wsm, num);
+}
+template <class G, int r, int rend, int NPY>
+struct RowsCT {
+  static __device__ __forceinline__ void run(const float* __restrict__ col, int base, const float* __restrict__ wsm,
+                                             float2 (&num)[NPY][kPX][2]) {
+    ring_row_ct<G, r, NPY>(col, base, wsm, num);
+    RowsCT<G, r + 1, rend, NPY>::run(col, base, wsm, num);
+  }
+};
+template <class G, int rend, int NPY>
+struct RowsCT<G, rend, rend, NPY> {
+  static __device__ __forceinline__ void run(const float*, int, const float*, float2 (&)[NPY][kPX][2]) {}
+};
+template <class G, int NPY>
+__device__ __forceinline__ void ring_stream(const float* __restrict__ col, int base, const float* __restrict__ wsm,
+                                            float2 (&num)[NPY][kPX][2]) {
+  constexpr int R = G::RR, K1 = 2 * R + 1;
+  constexpr int NC = kPX + 2 * R;
+  constexpr int NR = NPY + 2 * R;
+  if constexpr (2 * R < NPY - 1) {
+    RowsCT<G, 0, NR, NPY>::run(col, base, wsm, num);
+  } else {
+    RowsCT<G, 0, NPY - 1, NPY>::run(col, base, wsm, num);  // head rows
+    int s = base + NPY - 1;
+    if (s >= G::NSLOT) s -= G::NSLOT;
+    float4 head[kPX];  // the first kPX columns of the loop's next row, loaded one row ahead
+    {
+      const float* rp = col + s * (G::SC * kDB);
+#pragma unroll
+      for (int j = 0; j < kPX; ++j) head[j] = *reinterpret_cast<const float4*>(rp + j * kDB);
+    }
+#pragma unroll 1
+    for (int r = NPY - 1; r <= 2 * R; ++r) {  // full rows: every output row pyl, dy = r - pyl
+      const float* rp = col + s * (G::SC * kDB);
+      if (++s >= G::NSLOT) s -= G::NSLOT;
+      float4 c[NC];
+#pragma unroll
+      for (int j = 0; j < kPX; ++j) c[j] = head[j];
+#pragma unroll
+      for (int j = kPX; j < NC; ++j) c[j] = *reinterpret_cast<const float4*>(rp + j * kDB);
+      {  // next row's head (the row after the loop is a tail row or, for ρ's last row, harmless)
+        const float* rn = col + s * (G::SC * kDB);
+#pragma unroll
+        for (int j = 0; j < kPX; ++j) head[j] = *reinterpret_cast<const float4*>(rn + j * kDB);
+      }
+      const float* wr = wsm + r * K1 * kPX;  // (pyl, dy = r - pyl) -> wr + pyl (K1 - 1) K1 kPX
+#pragma unroll
+      for (int dx = 0; dx < K1; ++dx) {
+#pragma unroll
+        for (int pyl = 0; pyl < NPY; ++pyl) {
+          const float4 w = reinterpret_cast<const float4*>(wr + pyl * (K1 - 1) * K1 * kPX)[dx];
+          const float wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int px = 0; px < kPX; ++px) {
+            const float4 cc = c[dx + px];
+            ffma2(num[pyl][px][0], wv[px], make_float2(cc.x, cc.y));
+            ffma2(num[pyl][px][1], wv[px], make_float2(cc.z, cc.w));
+          }
+        }
+      }
+    }
+    RowsCT<G, 2 * R + 1, NR, NPY>::run(col, base, wsm, num);  // tail rows
+  }
+}
+
 // GENERAL: explicit numerator and denominator of one output row.
-template <int R>
+template <class G>
 __device__ __forceinline__ void ring_num_den_row(const float* __restrict__ col, int base, const float* __restrict__ wrow,
                                                  float2 (&num)[kPX][2], float2 (&den)[kPX][2]) {
-  using G = WGeo<R>;
+  constexpr int R = G::RR;
   constexpr int K1 = 2 * R + 1;
   constexpr int NC = kPX + 2 * R;
   constexpr int RS = G::SC * kDB;
@@ -349,7 +456,7 @@ __device__ __forceinline__ void ring_num_den_row(const float* __restrict__ col, 
 #pragma unroll 1
   for (int dy = 0; dy < K1; ++dy) {
     int s = base + dy;
-    if (s >= G::SR) s -= G::SR;
+    if (s >= G::NSLOT) s -= G::NSLOT;
     const float* rp = col + s * RS;
     float4 c[NC];
 #pragma unroll
@@ -372,25 +479,32 @@ __device__ __forceinline__ void ring_num_den_row(const float* __restrict__ col, 
   }
 }
 
-// Issue the TMA loads of one walker phase (thread 0): rows [yc, yc + SROWS) of
-// the strip's packed columns / statistics and of the other image's range; for
-// a step also the guide tile (buffer gb).  Completion: sm.bar (one phase).
-template <int R>
-__device__ __forceinline__ void walk_issue(const WalkArgs& a, WSmem<R>& sm, int f, int side, int strip, int b, int yc,
-                                           int y0, bool step, int gb) {
-  using G = WGeo<R>;
+// Issue the TMA loads of one walker phase (one thread): rows [yc, yc + G::SROWS)
+// of the strip's packed columns / statistics and of the other image's range;
+// with gdst also the guide tile of output rows [y0, y0 + G::GH - 2R).
+// Completion: bar (one phase, expect_tx).
+template <class G>
+__device__ __forceinline__ void walk_issue_g(const WalkArgs& a, uint32_t* Ps, int2* Ss, uint32_t* Po, int2* So,
+                                             float* gdst, unsigned long long* bar, int f, int side, int strip, int b,
+                                             int yc, int y0) {
+  constexpr int R = G::RR;
   constexpr unsigned kStageBytes = G::SROWS * (G::SPC * 4 + G::SSC * 8 + G::OPC * 4 + G::OSC * 8);
   constexpr unsigned kGuideBytes = G::GH * G::GWS * 4;
   const int x0 = strip * G::TX;
   const int dlo = a.d_min + b * kDB;
   const int obase = side == 0 ? x0 - R - dlo - 63 : x0 - R + dlo;
   fence_proxy_async();
-  mbar_expect_tx(&sm.bar, kStageBytes + (step ? kGuideBytes : 0u));
-  tma_load_3d(sm.Ps, &a.tmPs[side], &sm.bar, (x0 - R - 1) & ~3, yc, f);
-  tma_load_3d(sm.Ss, &a.tmSs[side], &sm.bar, (2 * (x0 - R)) & ~3, yc, f);  // (S, r) word pairs
-  tma_load_3d(sm.Po, &a.tmPo[1 - side], &sm.bar, (obase - 1) & ~3, yc, f);
-  tma_load_3d(sm.So, &a.tmSo[1 - side], &sm.bar, (2 * obase) & ~3, yc, f);
-  if (step) tma_load_3d(sm.g[gb], &a.tmG[side], &sm.bar, x0, y0, f);  // padded coordinates: frame (x0-R, y0-R)
+  mbar_expect_tx(bar, kStageBytes + (gdst ? kGuideBytes : 0u));
+  tma_load_3d(Ps, &a.tmPs[side], bar, (x0 - R - 1) & ~3, yc, f);
+  tma_load_3d(Ss, &a.tmSs[side], bar, (2 * (x0 - R)) & ~3, yc, f);  // (S, r) word pairs
+  tma_load_3d(Po, &a.tmPo[1 - side], bar, (obase - 1) & ~3, yc, f);
+  tma_load_3d(So, &a.tmSo[1 - side], bar, (2 * obase) & ~3, yc, f);
+  if (gdst) tma_load_3d(gdst, &a.tmG[side], bar, x0, y0, f);  // padded coordinates: frame (x0-R, y0-R)
+}
+template <int R>
+__device__ __forceinline__ void walk_issue(const WalkArgs& a, WSmem<R>& sm, int f, int side, int strip, int b, int yc,
+                                           int y0, bool step, int gb) {
+  walk_issue_g<WGeo<R>>(a, sm.Ps, sm.Ss, sm.Po, sm.So, step ? sm.g[gb] : nullptr, &sm.bar, f, side, strip, b, yc, y0);
 }
 
 // grid: min(total steps, #SMs) CTAs; block 256; one CTA per SM.
@@ -477,7 +591,7 @@ __global__ void __launch_bounds__(256, 1) k_fbs(const __grid_constant__ WalkArgs
         const int sy = y0 + wy;
         const int gb = nstep & 1;
         // classification words of this (sub-tile, d-block), in flight during the cost phase
-        const WCw<R> cw(a.W, a.H, a.d_min, a.d_max, side, sx, sy, b);
+        const WCw<G> cw(a.W, a.H, a.d_min, a.d_max, side, sx, sy, b);
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
           const int i = lane + 32 * k, row = i >> 2, wd = i & 3;
@@ -618,7 +732,7 @@ __global__ void __launch_bounds__(256, 1) k_fbs(const __grid_constant__ WalkArgs
 #pragma unroll
             for (int jj = 0; jj < kPX; ++jj) head[jj] = *reinterpret_cast<const float4*>(rp + jj * kDB);
           }
-          if (!(FBS_ABL & 2)) RingRows<R, 0, HPY + 2 * R, HPY>::run(col, base, wsm, head, num);
+          if (!(FBS_ABL & 2)) RingRows<G, 0, HPY + 2 * R, HPY>::run(col, base, wsm, head, num);
           __syncwarp();  // every lane is done with the weights before the dead rows are overwritten
 #pragma unroll
           for (int pyl = 0; pyl < HPY; ++pyl)
@@ -660,7 +774,7 @@ __global__ void __launch_bounds__(256, 1) k_fbs(const __grid_constant__ WalkArgs
             float2 num[kPX][2], den[kPX][2];
             int bb = base + pyl;
             if (bb >= G::SR) bb -= G::SR;
-            ring_num_den_row<R>(col, bb, wsm + pyl * RS, num, den);
+            ring_num_den_row<G>(col, bb, wsm + pyl * RS, num, den);
             __syncwarp();
 #pragma unroll
             for (int px = 0; px < kPX; ++px) {

@@ -39,6 +39,7 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 constexpr float kSent = -2.0f;   // undefined aggregated cost / exported cost (R#7)
 constexpr float kUndef = -0.0f;  // undefined cost in the cost ring (never a defined NCC value)
 constexpr int kMaxRadius = 6;    // FBS_MAX_RADIUS
+constexpr int kWsMaxRadius = 4;  // radii run by the warp-specialised walker (fbs_ws.cuh)
 // Smallest tap weight the handle accepts, as -log2 (FBS_MAX_WEIGHT_EXP2, R#13):
 // 2^-124 stays a normal fp32 after ex2.approx.ftz and any rounding of the exponent.
 constexpr double kMaxWeightExp2 = 124.0;
@@ -188,6 +189,24 @@ __device__ __forceinline__ unsigned long long wta_butterfly16(unsigned long long
     }
   }
   return k[0];
+}
+
+// The same for 8 slots (2 x 4 pixels per half-warp): the transposing butterfly
+// within each group of 8 lanes, then the two groups of a half combined
+// (4+2+1+1 = 8 u64 shuffles); afterwards lanes l and l ^ 8 hold slot l & 7.
+__device__ __forceinline__ unsigned long long wta_butterfly8(unsigned long long (&k)[8], int lane) {
+#pragma unroll
+  for (int lvl = 0; lvl < 3; ++lvl) {
+    const int n = 4 >> lvl;
+    const bool up = lane & n;
+#pragma unroll
+    for (int i = 0; i < n; ++i) {
+      const unsigned long long keep = up ? k[n + i] : k[i];
+      const unsigned long long send = up ? k[i] : k[n + i];
+      k[i] = umax64(keep, shfl_xor64(send, n));
+    }
+  }
+  return umax64(k[0], shfl_xor64(k[0], 8));
 }
 
 // ---------------------------------------------------------------------------

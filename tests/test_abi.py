@@ -54,11 +54,14 @@ def sass_of(function: str) -> str:
 
 
 def test_sass_uses_ffma2_tma_dp4a():
-    """The fused kernel (radius 4): the aggregation stream issues FFMA2 with a
-    broadcast scalar weight (fully unrolled: 4x6 px x 81 taps per warp), the
-    cost rows are staged by TMA (UTMALDG) and the 3x3 dot products use DP4A."""
-    out = sass_of("_ZN3fbs5k_fbsILi4ELb0EEEvNS_8WalkArgsE")
-    assert out.count("FFMA2") >= 24 * 81
+    """The fused warp-specialised kernel (radius 4): the aggregation stream issues
+    FFMA2 with a broadcast scalar weight (a cost-row loop whose body feeds 2 output
+    rows x 4 px x 9 taps x 2 disparity pairs), the cost rows are staged by TMA
+    (UTMALDG), the 3x3 dot products use DP4A and the hand-over between producer
+    and consumer warps uses mbarriers (SYNCS)."""
+    out = sass_of("_ZN3fbs8k_fbs_wsILi4ELb0EEEvNS_8WalkArgsE")
+    assert out.count("FFMA2") >= 2 * 4 * 9 * 2
+    assert "SYNCS" in out
     assert re.search(r"FFMA2 R\d+, R\d+\.F32, R\d+\.F32x2", out)
     assert "UTMALDG" in out
     assert "IDP.4A" in out or "IDP4A" in out

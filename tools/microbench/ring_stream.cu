@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_ring(int reps, float* out) {
     float4 head[kPX];
 #pragma unroll
     for (int j = 0; j < kPX; ++j) head[j] = *reinterpret_cast<const float4*>(col + base * G::SC * kDB + j * kDB);
-    RingRows<R, 0, HPY + 2 * R, HPY>::run(col, base, wsm, head, num);
+    RingRows<G, 0, HPY + 2 * R, HPY>::run(col, base, wsm, head, num);
 #pragma unroll
     for (int py = 0; py < HPY; ++py)
 #pragma unroll
