@@ -152,6 +152,19 @@ def load_traffic(cfgname, path):
         return None
 
 
+def bench_config(cfg, world):
+    """The `config` object of the JSON line — identical for both arms (the driver
+    compares them): the workload, its partition across ranks and the inputs."""
+    banded = cfg.name == "mb2014"
+    return {"workload": f"{cfg.name} {cfg.W}x{cfg.H} d={cfg.d_min}..{cfg.d_max} (D={cfg.D}) "
+                        f"rho={cfg.radius} gamma_d={cfg.gamma_d} gamma_r={cfg.gamma_r}",
+            "frames_per_step_per_rank": 1,
+            "partition": (f"row bands x{world} + NCCL all-gather" if banded else
+                          f"frame sharding x{world}, no data-path collective"),
+            "l2": "256 MiB L2 flush between timed steps (outside the step events)",
+            "input_sha256": synth.digest(*synth.frame(cfg, 0))[:16]}
+
+
 # ---------------------------------------------------------------------------
 def run_ours(args, cfg, rank, world, local_rank):
     import torch
@@ -166,7 +179,10 @@ def run_ours(args, cfg, rank, world, local_rank):
     frames_np = [synth.frame(cfg, i + (0 if banded else 1000 * rank)) for i in range(nfr)]
     Ls = [torch.from_numpy(L).to(dev) for L, _ in frames_np]
     Rs = [torch.from_numpy(R).to(dev) for _, R in frames_np]
-    m = fbs.FBS(cfg.W, cfg.H, cfg.d_min, cfg.d_max, cfg.radius, cfg.gamma_d, cfg.gamma_r, path=args.path)
+    # row bands (N > 1): each rank's handle covers only its band (fbs_create_band)
+    band = fdist.band_range(cfg.H, rank, world) if banded and world > 1 else None
+    m = fbs.FBS(cfg.W, cfg.H, cfg.d_min, cfg.d_max, cfg.radius, cfg.gamma_d, cfg.gamma_r, path=args.path,
+                rows=band if band and band[1] > band[0] else None)
     out = torch.empty((cfg.H, cfg.W), dtype=torch.float32, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
@@ -183,6 +199,28 @@ def run_ours(args, cfg, rank, world, local_rank):
         step(i)
     torch.cuda.synchronize()
     launches = m.launches_per_frame()
+    # the timed steps replay CUDA graphs of fbs_compute (one per input frame; SURVEY
+    # §8(d)): fbs_compute only enqueues, so it captures as is
+    graphs = []
+    if not banded and not args.no_graph:
+        cs = torch.cuda.Stream()
+        cs.wait_stream(stream)
+        with torch.cuda.stream(cs):
+            for i in range(nfr):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=cs):
+                    m.compute(Ls[i], Rs[i], out=out, stream=cs)
+                graphs.append(g)
+        torch.cuda.synchronize()
+        for i in range(args.warmup):
+            graphs[i % nfr].replay()
+        torch.cuda.synchronize()
+
+    def timed_step(i):
+        if graphs:
+            graphs[i % nfr].replay()
+        else:
+            step(i)
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     if world > 1:
@@ -194,7 +232,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         for i in range(args.steps):
             flush.fill_(float(i))            # untimed L2 flush (256 MiB > 126 MB L2)
             ev[i][0].record(stream)
-            step(i)
+            timed_step(i)
             ev[i][1].record(stream)
         torch.cuda.synchronize()
     t_wall = time.perf_counter() - t_wall
@@ -246,10 +284,25 @@ def run_ours(args, cfg, rank, world, local_rank):
         e_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in e_ev)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        # single-frame latency of the blocking host call (wall clock around
+        # fbs_compute_host: upload, compute, download, synchronise), L2 flushed before each
+        h1l, h1r = hl[0].clone().pin_memory(), hr[0].clone().pin_memory()
+        h1o = torch.empty((cfg.H, cfg.W), dtype=torch.float32).pin_memory()
+        lat = []
+        for i in range(3 + 50):
+            flush.fill_(float(i))
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            m.compute_host(h1l, h1r, out=h1o, stream=stream)
+            if i >= 3:
+                lat.append(time.perf_counter() - t0)
         e2e = {"value": mdisp(cfg, ne * EB * world, float(e_ms.item()) / 1e3), "unit": "Mdisp/s",
                "h2d_bytes_per_step": 2 * cfg.W * cfg.H * EB, "d2h_bytes_per_step": 4 * cfg.W * cfg.H * EB,
                "frames_per_step": EB, "fps": ne * EB * world / (float(e_ms.item()) / 1e3),
-               "api": "fbs_compute_host_batch (pinned host buffers, pipelined copies)"}
+               "api": "fbs_compute_host_batch (pinned host buffers, pipelined copies; the step's first "
+                      "upload starts after the step's start event)",
+               "single_frame_latency_ms": round(1e3 * statistics.median(lat), 4),
+               "single_frame_api": "fbs_compute_host, one frame, blocking, wall clock (median of 50)"}
 
     if rank != 0:
         return None
@@ -297,13 +350,9 @@ def run_ours(args, cfg, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (seeded layered Middlebury-like pairs, stereo_synth v%d)" % synth.SYNTH_VERSION,
-        "config": {"workload": f"{cfg.name} {cfg.W}x{cfg.H} d={cfg.d_min}..{cfg.d_max} (D={cfg.D}) "
-                               f"rho={cfg.radius} gamma_d={cfg.gamma_d} gamma_r={cfg.gamma_r}",
-                   "frames_per_step_per_rank": 1,
-                   "partition": (f"row bands x{world} + NCCL all-gather" if banded else
-                                 f"frame sharding x{world}, no data-path collective"),
-                   "l2": "256 MiB L2 flush between timed steps (outside the step events)",
-                   "input_sha256": synth.digest(*frames_np[0])[:16]},
+        "config": bench_config(cfg, world),
+        "path": args.path,
+        "timing": ("CUDA-graph replay of fbs_compute per step" if graphs else "eager launches per step"),
         "roofline": roof,
         "cpu_baseline": base,
         "e2e": e2e,
@@ -344,14 +393,13 @@ def run_reference(args, cfg, rank):
     for i in range(args.steps):
         tt += band_step((i * B) % max(1, cfg.H - B), B)
     value = cfg.W * B * cfg.D * args.steps / tt * 1e-6
-    sample = (f"per step: oracle on a {B}-row band (+{halo}-row halo) of a {cfg.name} "
-              f"{cfg.W}x{cfg.H} D={cfg.D} frame, {th} threads")
+    sample = (f"per step: oracle on a {B}-row band (+{halo}-row halo) of the same {cfg.name} "
+              f"{cfg.W}x{cfg.H} D={cfg.D} frame (frame 0 of the config), {th} threads")
     return {"metric": "Mdisp/s", "value": round(value, 3), "unit": "Mdisp/s", "n_gpus": 0,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tt / args.steps * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{cfg.name} {cfg.W}x{cfg.H} d={cfg.d_min}..{cfg.d_max} (D={cfg.D}) "
-                                   f"rho={cfg.radius}", "band_rows": B},
+            "config": bench_config(cfg, int(os.environ.get("WORLD_SIZE", "1"))),
             "cpu_baseline": {"value": round(value, 3), "unit": "Mdisp/s", "cores": th, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": round(value, 3), "unit": "Mdisp/s", "h2d_bytes_per_step": 0,
@@ -371,6 +419,8 @@ def main():
                     help="frames per end-to-end step (fbs_compute_host_batch pipeline depth)")
     ap.add_argument("--radius", type=int, default=None,
                     help="override the config's aggregation radius rho (NEXT-1 sweep; paper's operating point is 6)")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="time eager launches instead of CUDA-graph replays")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the e2e and cpu_baseline legs (for profiler runs)")
     args = ap.parse_args()

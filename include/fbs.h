@@ -100,6 +100,15 @@ fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, float sigma_
 fbs_ctx* fbs_create_ex(int W, int H, int d_min, int d_max, int radius, float sigma_s, float sigma_r,
                        int path);
 
+/* fbs_create_band — a handle that serves only output rows [row_begin, row_end)
+ * through fbs_compute_rows (the row-band partitioner's per-rank handle, DESIGN.md
+ * §7): its cost volumes and left aggregated store cover just those rows plus the
+ * tile / halo rows they need, so per-rank memory shrinks with the number of bands.
+ * fbs_compute, _batch, _host* and the debug calls return FBS_E_ARG on it.
+ * 0 <= row_begin < row_end <= H, else NULL. */
+fbs_ctx* fbs_create_band(int W, int H, int d_min, int d_max, int radius, float sigma_s, float sigma_r,
+                         int path, int row_begin, int row_end);
+
 /* fbs_destroy — free the handle and its scratch.  The caller must have
  * synchronised all work enqueued with it.  NULL is a no-op. */
 void fbs_destroy(fbs_ctx* h);
@@ -125,9 +134,12 @@ int fbs_compute(fbs_ctx* h, const uint8_t* left, const uint8_t* right, float* di
 /*
  * fbs_compute_rows — rows [row_begin, row_end) of what fbs_compute would write,
  * bit-identical to them.  left/right are the FULL frames (device); disp_band
- * is device float [(row_end-row_begin)][W].  Reads input rows
- * [row_begin-ρ-1, row_end+ρ+1) only.  Used by the row-band multi-GPU
- * partitioner.  0 <= row_begin < row_end <= H, else FBS_E_ARG.
+ * is device float [(row_end-row_begin)][W].  Reads the input rows of the
+ * aggregation tiles that cover the band plus their halo:
+ * [floor(row_begin/T)*T - ρ - 1, ceil(row_end/T)*T + ρ + 1) clipped to the frame,
+ * T = the path's tile height (≤ 12 rows).  Used by the row-band multi-GPU
+ * partitioner.  rb0 <= row_begin < row_end <= rb1 (the handle's
+ * rows: [0, H), or fbs_create_band's), else FBS_E_ARG.
  */
 int fbs_compute_rows(fbs_ctx* h, const uint8_t* left, const uint8_t* right, int row_begin,
                      int row_end, float* disp_band, fbs_stream_t stream);

@@ -26,7 +26,7 @@ FBS_PATH_VOLUME, FBS_PATH_FUSED = 0, 1
 PATHS = {"volume": FBS_PATH_VOLUME, "fused": FBS_PATH_FUSED}
 
 # every symbol include/fbs.h declares
-EXPORTS = ("fbs_create", "fbs_create_ex", "fbs_destroy", "fbs_last_error", "fbs_compute", "fbs_compute_rows",
+EXPORTS = ("fbs_create", "fbs_create_ex", "fbs_create_band", "fbs_destroy", "fbs_last_error", "fbs_compute", "fbs_compute_rows",
            "fbs_compute_batch", "fbs_compute_host", "fbs_compute_host_batch", "fbs_debug_volumes", "fbs_debug_select",
            "fbs_debug_maps", "fbs_stats", "fbs_profile_enable", "fbs_profile_read", "fbs_tile_stats")
 FBS_NSTAGES = 3
@@ -54,6 +54,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.fbs_create.restype = P
     lib.fbs_create_ex.argtypes = [I, I, I, I, I, F, F, I]
     lib.fbs_create_ex.restype = P
+    lib.fbs_create_band.argtypes = [I, I, I, I, I, F, F, I, I, I]
+    lib.fbs_create_band.restype = P
     lib.fbs_destroy.argtypes = [P]
     lib.fbs_destroy.restype = None
     lib.fbs_last_error.argtypes = []
@@ -113,6 +115,14 @@ def fbs_create(W: int, H: int, d_min: int, d_max: int, radius: int, sigma_s: flo
 def fbs_create_ex(W: int, H: int, d_min: int, d_max: int, radius: int, sigma_s: float, sigma_r: float,
                   path: int):
     h = load_library().fbs_create_ex(W, H, d_min, d_max, radius, sigma_s, sigma_r, path)
+    if not h:
+        raise FbsError(FBS_E_PARAM, last_error())
+    return ctypes.c_void_p(h)
+
+
+def fbs_create_band(W: int, H: int, d_min: int, d_max: int, radius: int, sigma_s: float, sigma_r: float,
+                    path: int, row_begin: int, row_end: int):
+    h = load_library().fbs_create_band(W, H, d_min, d_max, radius, sigma_s, sigma_r, path, row_begin, row_end)
     if not h:
         raise FbsError(FBS_E_PARAM, last_error())
     return ctypes.c_void_p(h)
@@ -196,7 +206,7 @@ class FBS:
     on the handle's device: uint8 [H, W] pairs in, float32 [H, W] map out."""
 
     def __init__(self, W: int, H: int, d_min: int, d_max: int, radius: int, sigma_s: float,
-                 sigma_r: float, device=None, path: str = "volume"):
+                 sigma_r: float, device=None, path: str = "volume", rows=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_1807_02044_b200 needs a CUDA device (sm_100a); no CPU fallback")
@@ -207,8 +217,12 @@ class FBS:
         if path not in PATHS:
             raise ValueError(f"path must be one of {sorted(PATHS)}")
         self.path = path
+        self.rows = (0, H) if rows is None else (int(rows[0]), int(rows[1]))
         with torch.cuda.device(self.device):
-            self.h = fbs_create_ex(W, H, d_min, d_max, radius, sigma_s, sigma_r, PATHS[path])
+            if rows is None:
+                self.h = fbs_create_ex(W, H, d_min, d_max, radius, sigma_s, sigma_r, PATHS[path])
+            else:  # band handle: serves compute_rows within `rows` only (fbs_create_band)
+                self.h = fbs_create_band(W, H, d_min, d_max, radius, sigma_s, sigma_r, PATHS[path], *self.rows)
 
     def close(self):
         if getattr(self, "h", None):
@@ -257,8 +271,8 @@ class FBS:
 
     def compute_rows(self, left, right, r0: int, r1: int, out=None, stream=None):
         self._chk_pair(left, right)
-        if not 0 <= r0 < r1 <= self.H:
-            raise ValueError("compute_rows: need 0 <= r0 < r1 <= H")
+        if not self.rows[0] <= r0 < r1 <= self.rows[1]:
+            raise ValueError(f"compute_rows: need {self.rows[0]} <= r0 < r1 <= {self.rows[1]}")
         out = self._out(out, (r1 - r0, self.W))
         fbs_compute_rows(self.h, left, right, r0, r1, out, stream)
         return out

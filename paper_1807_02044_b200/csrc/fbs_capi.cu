@@ -49,6 +49,9 @@ struct fbs_ctx {
   // volume path scratch (fbs_volume.cuh): padded cost volumes [Hv][nblk][Wv][64] per side,
   // padded guides, block-defined masks, the left aggregated volume (multi-block frames)
   int Wv, Hv, vWb, vWg;
+  int rb0, rb1;        // rows this handle serves (band handles: fbs_create_band), else [0, H)
+  int vbase, abase;    // frame row of volume row R / of aggL row 0 (band handles), else 0
+  int arows;           // rows of aggL
   float *volL, *volR, *gpadL, *gpadR, *aggL;
   uint32_t *vbitsL, *vbitsR;
   // host path (fbs_compute_host[_batch]): two frame slots each, created on first use
@@ -192,6 +195,8 @@ static size_t frame_bytes(const fbs_ctx* h) {
 }
 
 static fbs_ctx* create_volume(fbs_ctx* h);
+static fbs_ctx* create_impl(int W, int H, int d_min, int d_max, int radius, float sigma_s, float sigma_r, int path,
+                            int rb0, int rb1);
 
 extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, float sigma_s, float sigma_r) {
   return fbs_create_ex(W, H, d_min, d_max, radius, sigma_s, sigma_r, FBS_PATH_VOLUME);
@@ -199,6 +204,20 @@ extern "C" fbs_ctx* fbs_create(int W, int H, int d_min, int d_max, int radius, f
 
 extern "C" fbs_ctx* fbs_create_ex(int W, int H, int d_min, int d_max, int radius, float sigma_s, float sigma_r,
                                   int path) {
+  return create_impl(W, H, d_min, d_max, radius, sigma_s, sigma_r, path, 0, H);
+}
+
+extern "C" fbs_ctx* fbs_create_band(int W, int H, int d_min, int d_max, int radius, float sigma_s, float sigma_r,
+                                    int path, int row_begin, int row_end) {
+  if (row_begin < 0 || row_end > H || row_begin >= row_end) {
+    g_err = "fbs_create_band: need 0 <= row_begin < row_end <= H";
+    return nullptr;
+  }
+  return create_impl(W, H, d_min, d_max, radius, sigma_s, sigma_r, path, row_begin, row_end);
+}
+
+static fbs_ctx* create_impl(int W, int H, int d_min, int d_max, int radius, float sigma_s, float sigma_r, int path,
+                            int rb0, int rb1) {
   g_err.clear();
   if (path != FBS_PATH_VOLUME && path != FBS_PATH_FUSED) {
     fail(FBS_E_PARAM, "fbs_create: path must be FBS_PATH_VOLUME or FBS_PATH_FUSED");
@@ -243,6 +262,7 @@ extern "C" fbs_ctx* fbs_create_ex(int W, int H, int d_min, int d_max, int radius
   }
   std::memset((void*)h, 0, sizeof(*h));
   h->path = path;
+  h->rb0 = rb0; h->rb1 = rb1;
   h->W = W; h->H = H; h->d_min = d_min; h->d_max = d_max; h->D = d_max - d_min + 1;
   h->nblk = (h->D + kDB - 1) / kDB;
   h->R = radius;
@@ -355,7 +375,13 @@ static fbs_ctx* create_volume(fbs_ctx* h) {
   h->TX = vol::kTX;
   h->TY = vol::agg_tile_h(R);
   h->Wv = (W + vol::kTX - 1) / vol::kTX * vol::kTX + 2 * R;
-  h->Hv = (H + vol::kTYMax - 1) / vol::kTYMax * vol::kTYMax + vol::kTYMax + 2 * R;
+  {  // rows of the served band [rb0, rb1): cost rows [vbase, ..), tile rows [abase, ..)
+    const int TY = h->TY, ty0 = h->rb0 / TY, ty1 = (h->rb1 + TY - 1) / TY;
+    h->vbase = std::max(0, ty0 * TY - R);
+    h->abase = ty0 * TY;
+    h->Hv = ty1 * TY + 2 * R - h->vbase + vol::kTYMax;
+    h->arows = std::min(H, ty1 * TY) - h->abase;
+  }
   h->vWb = (W + vol::kCX - 1) / vol::kCX * (vol::kCX / 32);
   h->vWg = vol::guide_pitch(W, R);
   const size_t npix = (size_t)W * H;
@@ -370,7 +396,7 @@ static fbs_ctx* create_volume(fbs_ctx* h) {
   ok &= cudaMalloc(&h->volR, nvol * 4) == cudaSuccess;
   ok &= cudaMalloc(&h->dmap[0], npix * 4) == cudaSuccess;
   ok &= cudaMalloc(&h->dmap[1], npix * 4) == cudaSuccess;
-  if (h->nblk > 1) ok &= cudaMalloc(&h->aggL, npix * h->nblk * kDB * sizeof(float)) == cudaSuccess;
+  if (h->nblk > 1) ok &= cudaMalloc(&h->aggL, (size_t)h->arows * W * h->nblk * kDB * sizeof(float)) == cudaSuccess;
   ok &= cudaMalloc(&h->agg3, npix * sizeof(float4)) == cudaSuccess;
   ok &= cudaMalloc(&h->tile_stats, 4 * sizeof(unsigned long long)) == cudaSuccess;
 #ifdef FBS_TRACE
@@ -494,7 +520,7 @@ static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0,
   {
     vol::CostArgs ca;
     ca.W = W; ca.H = H; ca.D = h->D; ca.d_min = h->d_min; ca.nblk = h->nblk; ca.Wv = h->Wv; ca.R = R;
-    ca.r0 = c0; ca.r1 = c1;
+    ca.r0 = c0; ca.r1 = c1; ca.vbase = h->vbase;
     ca.L = L; ca.Rimg = Rimg; ca.volL = h->volL; ca.volR = h->volR;
     ca.bitsL = h->vbitsL; ca.bitsR = h->vbitsR; ca.Wb = h->vWb;
     ca.gpadL = h->gpadL; ca.gpadR = h->gpadR; ca.Wg = h->vWg;
@@ -512,6 +538,7 @@ static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0,
   a.nkr = h->wa.nkr;
   a.gpadL = h->gpadL; a.gpadR = h->gpadR; a.Wg = h->vWg;
   a.r0 = r0; a.r1 = r1; a.ty0 = ty0;
+  a.vbase = h->vbase; a.abase = h->abase;
   a.volL = h->volL; a.volR = h->volR;
   a.bitsL = h->vbitsL; a.bitsR = h->vbitsR; a.Wb = h->vWb;
   a.dL = h->dmap[0]; a.dR = h->dmap[1]; a.aggL = h->aggL; a.exportR = aggR_exp;
@@ -522,6 +549,7 @@ static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0,
     if (cudaMalloc(&aggL_tmp, (size_t)W * H * kDB * sizeof(float)) != cudaSuccess)
       return fail(FBS_E_OOM, "fbs_debug_volumes: scratch");
     a.aggL = aggL_tmp;
+    a.abase = 0;
   }
   a.agg3 = (h->nblk == 1 && !aggL_exp) ? h->agg3 : nullptr;
   a.tile_stats = ev ? h->tile_stats : nullptr;
@@ -547,7 +575,7 @@ static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0,
     const dim3 grd((W + 127) / 128, r1 - r0);
     const cudaError_t e = launch_pdl(vol::k_finalize, grd, dim3(128), 0, s, (const int32_t*)h->dmap[0],
                                      (const int32_t*)h->dmap[1], (const float*)a.aggL, (const float4*)a.agg3,
-                                     h->nblk, W, r0, r1, h->d_min, h->d_max, out);
+                                     h->nblk, W, r0, r1, h->d_min, h->d_max, a.abase, out);
     if (e != cudaSuccess) return cuda_check(e, "k_finalize launch");
     h->launches += 1;
   }
@@ -620,23 +648,28 @@ static int run(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int nf, int r0
   return cuda_check(cudaGetLastError(), "fbs launch");
 }
 
+static bool full_frame(const fbs_ctx* h) { return h->rb0 == 0 && h->rb1 == h->H; }
+
 extern "C" int fbs_compute(fbs_ctx* h, const uint8_t* left, const uint8_t* right, float* disp_out,
                            fbs_stream_t stream) {
   if (!h || !left || !right || !disp_out) return fail(FBS_E_ARG, "fbs_compute: NULL argument");
+  if (!full_frame(h)) return fail(FBS_E_ARG, "fbs_compute: band handle (use fbs_compute_rows)");
   return run(h, left, right, 1, 0, h->H, disp_out, nullptr, nullptr, (cudaStream_t)stream);
 }
 
 extern "C" int fbs_compute_rows(fbs_ctx* h, const uint8_t* left, const uint8_t* right, int row_begin,
                                 int row_end, float* disp_band, fbs_stream_t stream) {
   if (!h || !left || !right || !disp_band) return fail(FBS_E_ARG, "fbs_compute_rows: NULL argument");
-  if (row_begin < 0 || row_end > h->H || row_begin >= row_end)
-    return fail(FBS_E_ARG, "fbs_compute_rows: need 0 <= row_begin < row_end <= H");
+  if (row_begin < h->rb0 || row_end > h->rb1 || row_begin >= row_end)
+    return fail(FBS_E_ARG, "fbs_compute_rows: need rb0 <= row_begin < row_end <= rb1 (the handle's rows; [0, H) "
+                           "unless created by fbs_create_band)");
   return run(h, left, right, 1, row_begin, row_end, disp_band, nullptr, nullptr, (cudaStream_t)stream);
 }
 
 extern "C" int fbs_compute_batch(fbs_ctx* h, const uint8_t* left, const uint8_t* right, int n,
                                  float* disp_out, fbs_stream_t stream) {
   if (!h || !left || !right || !disp_out) return fail(FBS_E_ARG, "fbs_compute_batch: NULL argument");
+  if (!full_frame(h)) return fail(FBS_E_ARG, "fbs_compute_batch: band handle");
   if (n < 1) return fail(FBS_E_ARG, "fbs_compute_batch: n must be >= 1");
   const size_t npix = (size_t)h->W * h->H;
   int launches = 0;
@@ -678,6 +711,7 @@ static int host_setup(fbs_ctx* h) {
 extern "C" int fbs_compute_host_batch(fbs_ctx* h, const uint8_t* left, const uint8_t* right, int n,
                                       float* disp_out, fbs_stream_t stream) {
   if (!h || !left || !right || !disp_out) return fail(FBS_E_ARG, "fbs_compute_host_batch: NULL argument");
+  if (!full_frame(h)) return fail(FBS_E_ARG, "fbs_compute_host_batch: band handle");
   if (n < 1) return fail(FBS_E_ARG, "fbs_compute_host_batch: n must be >= 1");
   int rc = host_setup(h);
   if (rc) return rc;
@@ -723,6 +757,7 @@ extern "C" int fbs_debug_volumes(fbs_ctx* h, const uint8_t* left, const uint8_t*
                                  float* cost_r, float* agg_l, float* agg_r, float* disp_out, int32_t* disp_l,
                                  int32_t* disp_r, fbs_stream_t stream) {
   if (!h || !left || !right) return fail(FBS_E_ARG, "fbs_debug_volumes: NULL argument");
+  if (!full_frame(h)) return fail(FBS_E_ARG, "fbs_debug_volumes: band handle");
   cudaStream_t s = (cudaStream_t)stream;
   const size_t npix = (size_t)h->W * h->H;
   float* tmp = nullptr;
@@ -759,6 +794,7 @@ extern "C" int fbs_debug_select(fbs_ctx* h, const float* agg_l, const float* agg
 extern "C" int fbs_debug_maps(fbs_ctx* h, const uint8_t* left, const uint8_t* right, float* disp_out,
                               int32_t* disp_l, int32_t* disp_r, fbs_stream_t stream) {
   if (!h || !left || !right || !disp_out) return fail(FBS_E_ARG, "fbs_debug_maps: NULL argument");
+  if (!full_frame(h)) return fail(FBS_E_ARG, "fbs_debug_maps: band handle");
   cudaStream_t s = (cudaStream_t)stream;
   const size_t npix = (size_t)h->W * h->H;
   int rc = run(h, left, right, 1, 0, h->H, disp_out, nullptr, nullptr, s);

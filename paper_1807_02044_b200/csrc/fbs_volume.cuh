@@ -75,6 +75,7 @@ __host__ __device__ __forceinline__ size_t vol_at(int vy, int b, int vx, int nbl
 // Stage 1+2: block statistics fused with the twin NCC cost volumes.
 struct CostArgs {
   int W, H, D, d_min, nblk, Wv, R, r0, r1, Wb;  // [r0, r1): cost rows; Wb = words per mask row
+  int vbase;                                     // frame row of volume row R (0; band handles: first cost row)
   const uint8_t *L, *Rimg;
   float *volL, *volR;
   uint32_t *bitsL, *bitsR;                      // block-defined masks, bit-packed [H][Wb]
@@ -167,7 +168,7 @@ __device__ __forceinline__ void cost_side(const CostArgs& a, unsigned char* smra
   const int xw = warp * PPW;
   const int npx = min(PPW, a.W - (x0 + xw));
   if (npx <= 0) return;
-  float* vp = vol + vol_at(y + a.R, 0, x0 + xw + a.R, a.nblk, a.Wv) + 2 * lane;
+  float* vp = vol + vol_at(y + a.R - a.vbase, 0, x0 + xw + a.R, a.nblk, a.Wv) + 2 * lane;
   const size_t bstride = (size_t)a.Wv * kDB;  // next d-block of the same pixel
   const uint32_t* cPs = cP + xw;               // self column of block xw + m: cPs[m .. m+2]
   const int2* sSR = bSR + xw;
@@ -267,7 +268,7 @@ __device__ __forceinline__ float finalize_pixel(int d_int, int e, float c0, floa
 // [H][nblk][W][64] store
 __global__ void k_finalize(const int32_t* __restrict__ dl, const int32_t* __restrict__ dr,
                            const float* __restrict__ aggL, const float4* __restrict__ agg3, int nblk, int W,
-                           int r0, int r1, int d_min, int d_max, float* __restrict__ out) {
+                           int r0, int r1, int d_min, int d_max, int abase, float* __restrict__ out) {
   pdl_wait();  // k_agg's maps
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = r0 + blockIdx.y;
@@ -281,7 +282,7 @@ __global__ void k_finalize(const int32_t* __restrict__ dl, const int32_t* __rest
     const float4 v = agg3[p];
     cm = v.x; c0 = v.y; cp = v.z;
   } else if (d >= 0) {
-    auto at = [&](int di) { return aggL[(((size_t)y * nblk + di / kDB) * W + x) * kDB + di % kDB]; };
+    auto at = [&](int di) { return aggL[(((size_t)(y - abase) * nblk + di / kDB) * W + x) * kDB + di % kDB]; };
     const int di = d - d_min;
     c0 = at(di);
     if (d > d_min) cm = at(di - 1);
@@ -320,6 +321,7 @@ __global__ void k_export_agg(const float* __restrict__ aggL, int W, int H, int D
 // form a pixel gets never depends on the row band being computed.
 struct AggArgs {
   int W, H, D, d_min, d_max, nblk, Wv, r0, r1;  // output rows [r0, r1)
+  int vbase, abase;               // frame rows of volume row R and of aggL row 0 (0 for full-frame handles)
   int ty0;                       // first tile row (tiles anchored at multiples of the tile height)
   const float *volL, *volR;      // cost volumes (padded layout)
   const float *gpadL, *gpadR;    // padded guide images (Eq.(8); the right image guides the right volume, R#11)
@@ -721,7 +723,7 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
   unsigned long long best = 0ull;  // running best key of slot (lane & 15) of this half
   for (int b = 0; b < a.nblk; ++b) {
     // volume row (sy + py0 - R + r) + R = sy + py0 + r; column (sx - R + j) + R = sx + j
-    const float* vb = vol + vol_at(sy + py0, b, sx, a.nblk, a.Wv) + 4 * dq;
+    const float* vb = vol + vol_at(sy + py0 - a.vbase, b, sx, a.nblk, a.Wv) + 4 * dq;
     if (b > 0) {  // this d-block's words (issued one d-block ahead)
       cp_async_wait_all();
       // one CTA barrier per d-block keeps the warps in lockstep: warps that drift
@@ -759,7 +761,7 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
         if (a.agg3)  // its weight row is dead: the stream of half-row pyl is done
           *reinterpret_cast<float4*>(vrow(pyl) + px * kDB + 4 * dq) = agg;
         else if (x < a.W && y < a.H)
-          *reinterpret_cast<float4*>(a.aggL + (((size_t)y * a.nblk + b) * a.W + x) * kDB + 4 * dq) = agg;
+          *reinterpret_cast<float4*>(a.aggL + (((size_t)(y - a.abase) * a.nblk + b) * a.W + x) * kDB + 4 * dq) = agg;
       } else if ((EXPORT ? a.exportR : nullptr) && x < a.W && y >= a.r0 && y < a.r1) {
         float* er = (EXPORT ? a.exportR : nullptr) + ((size_t)y * a.W + x) * a.D;
         const float av[4] = {agg.x, agg.y, agg.z, agg.w};
@@ -811,7 +813,7 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
         for (int s2 = 0; s2 < kPX * HPY; ++s2) {
           const int y = sy + py0 + s2 / kPX, x = sx + s2 % kPX;
           if (x < a.W && y < a.H)
-            *reinterpret_cast<float4*>(a.aggL + (((size_t)y * a.nblk + b) * a.W + x) * kDB + 4 * dq) =
+            *reinterpret_cast<float4*>(a.aggL + (((size_t)(y - a.abase) * a.nblk + b) * a.W + x) * kDB + 4 * dq) =
                 make_float4(kSent, kSent, kSent, kSent);
         }
       } else if (side == 1 && (EXPORT ? a.exportR : nullptr)) {

@@ -355,3 +355,31 @@ def test_paths_agree_on_maps(fbs):
     assert np.mean(l0 == l1) > 0.999 and np.mean(r0 == r1) > 0.999
     same = (l0 == l1)
     assert np.max(np.abs(o0 - o1)[same & (o0 >= 0) & (o1 >= 0)], initial=0) < 1e-3
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_band_handles(fbs, path):
+    """fbs_create_band handles (per-rank scratch of the row-band partitioner)
+    give the same bytes as the full-frame handle's fbs_compute_rows, allocate
+    less device memory, and refuse rows outside their band."""
+    cfg = synth.CONFIGS["kitti"]
+    L, R = (to_dev(x) for x in synth.frame(cfg, 0))
+    full = fbs.FBS(cfg.W, cfg.H, cfg.d_min, cfg.d_max, cfg.radius, cfg.gamma_d, cfg.gamma_r, path=path)
+    ref = full.compute(L, R).cpu().numpy()
+    del full
+    torch.cuda.synchronize()
+    for a, b in ((0, 94), (94, 188), (188, 281), (281, 375), (100, 101)):
+        before = torch.cuda.mem_get_info()[0]
+        m = fbs.FBS(cfg.W, cfg.H, cfg.d_min, cfg.d_max, cfg.radius, cfg.gamma_d, cfg.gamma_r, path=path,
+                    rows=(a, b))
+        used = before - torch.cuda.mem_get_info()[0]
+        got = m.compute_rows(L, R, a, b).cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), ref[a:b].view(np.uint32)), (a, b)
+        with pytest.raises(Exception):  # one row outside the band
+            m.compute_rows(L, R, a - 1, b) if a > 0 else m.compute_rows(L, R, a, b + 1)
+        with pytest.raises(Exception):
+            m.compute(L, R)
+        if path == "volume" and b - a < cfg.H // 2:
+            # volumes + left store cover the band, not the frame (2 x 375-row volumes ~ 0.9 GB)
+            assert used < 0.6e9, used
+        m.close()
