@@ -291,7 +291,12 @@ static fbs_ctx* create_impl(int W, int H, int d_min, int d_max, int radius, floa
   for (int dy = -radius; dy <= radius; ++dy)
     for (int dx = -radius; dx <= radius; ++dx)
       h->wa.cd[(dy + radius) * K1 + (dx + radius)] = (float)(-l2e * (double)(dx * dx + dy * dy) / (gd * gd));
-  h->wa.nkr = (float)(-l2e / (gr * gr));
+  // Taps of undefined blocks carry the guide offset kGuideFlag = 2^23 and must get
+  // weight +0 (2^(nkr (2^23 - 255)^2) < 2^-126, flushed by ex2.approx.ftz): this needs
+  // nkr <= -2e-12, i.e. gamma_r <= 8.5e5.  Larger gamma_r use nkr = -2e-12: every
+  // range weight is then within 9e-8 (relative) of Eq.(8)'s, below the error of
+  // ex2.approx itself (R#13).
+  h->wa.nkr = (float)std::min(-l2e / (gr * gr), -2e-12);
   if (path == FBS_PATH_VOLUME) return create_volume(h);
 
   const size_t F = h->fcap, npix = (size_t)W * H;

@@ -635,7 +635,6 @@ __global__ void __launch_bounds__(256, 1) k_fbs(const __grid_constant__ WalkArgs
                 asm("ex2.approx.ftz.f32 %0, %1;"
                     : "=f"(w)
                     : "f"(__fmaf_rn(__fmul_rn(dd, dd), a.nkr, a.cd[dy * K1 + dx])));
-                w = gv[tt] < kGuideFlag ? w : 0.f;  // taps of undefined blocks / outside the frame
                 col[dx] = __fadd_rn(col[dx], w);
                 wsm[((py * K1 + dy) * K1 + dx) * kPX + px] = w;
               }

@@ -49,9 +49,10 @@ constexpr int kTYMax = 12;       // tallest walker step of any radius
 
 // Padded guide images (written by k_prep): i(q) as a float, with an R-pixel
 // margin of kGuideUndef outside the frame.  A pixel whose own block is
-// undefined stores i + kGuideFlag: as a tap q (value >= kGuideFlag) its weight
-// is forced to +0, and as a centre p its intensity is recovered exactly
-// (i + 2^23 is exact in fp32).
+// undefined stores i + kGuideFlag: as a tap q it is >= 2^23 - 255 away from any
+// intensity, so its weight 2^(nkr Δ² + cd) flushes to exactly +0 (nkr <= -2e-12,
+// see fbs_create), and as a centre p its intensity is recovered exactly (i + 2^23
+// is exact in fp32).
 constexpr float kGuideUndef = 1e30f;
 constexpr float kGuideFlag = 8388608.0f;
 __host__ __device__ constexpr int guide_pitch(int W, int R) { return ((W + 15) / 16 * 16 + 2 * R + 4 + 3) / 4 * 4; }

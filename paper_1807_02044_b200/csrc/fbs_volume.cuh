@@ -56,8 +56,8 @@ __host__ __device__ constexpr int agg_tile_h(int R) { return (R >= 6 ? 4 : kPYMa
 constexpr int kCX = FBS_KCX;     // cost kernel: pixels per CTA (multiple of 32)
 // Padded guide images for k_agg (written by k_cost): i(q) as a float, with an
 // R-pixel margin of kGuideUndef outside the frame.  A pixel whose own block is
-// undefined stores i + kGuideFlag: as a tap q (value >= kGuideFlag) its weight is
-// forced to +0 by an explicit select, and as a
+// undefined stores i + kGuideFlag: as a tap q it is >= 2^23 - 255 away from any
+// intensity, so its weight flushes to exactly +0 (nkr <= -2e-12, fbs_create), and as a
 // centre p its intensity is recovered exactly (i + 2^23 is exact in fp32).
 constexpr float kGuideUndef = 1e30f;
 constexpr float kGuideFlag = 8388608.0f;
@@ -678,7 +678,6 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
           const float dd = __fsub_rn(gv[t], gp);
           float w;
           asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(w) : "f"(__fmaf_rn(__fmul_rn(dd, dd), a.nkr, a.cd[dy * K1 + dx])));
-          w = gv[t] < kGuideFlag ? w : 0.f;  // taps of undefined blocks / outside the frame
           col[dx] = __fadd_rn(col[dx], w);
           wsm[((py * K1 + dy) * K1 + dx) * kPX + px] = w;
         }

@@ -154,7 +154,6 @@ __device__ __forceinline__ void ws_weights(const WalkArgs& a, const float* gtile
         const float dd = __fsub_rn(gv[dx], gp);
         float w;
         asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(w) : "f"(__fmaf_rn(__fmul_rn(dd, dd), a.nkr, a.cd[dy * K1 + dx])));
-        w = gv[dx] < kGuideFlag ? w : 0.f;  // taps of undefined blocks / outside the frame
         col[dx] = __fadd_rn(col[dx], w);
         wsm[((py * K1 + dy) * K1 + dx) * kPX + px] = w;
       }
