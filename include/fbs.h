@@ -71,6 +71,7 @@ typedef struct CUstream_st* fbs_stream_t;
  *   W, H          frame size in pixels (>= 3 each)
  *   d_min, d_max  inclusive disparity search range, 0 <= d_min < d_max
  *   radius        ρ of Eq.(6): aggregation window (2ρ+1)^2; supported 1..FBS_MAX_RADIUS
+ *                 (10; 6 on FBS_PATH_FUSED)
  *                 (0 is also accepted: the aggregation is then the identity)
  *   sigma_s       γ_d of Eq.(7), used verbatim as exp(-r^2/γ_d^2)   (> 0, finite)
  *   sigma_r       γ_r of Eq.(8), used verbatim as exp(-Δ^2/γ_r^2)   (> 0, finite)
@@ -116,8 +117,9 @@ void fbs_destroy(fbs_ctx* h);
 /* fbs_last_error — message of the last failing call on this thread ("" if none). */
 const char* fbs_last_error(void);
 
-/* Maximum supported aggregation radius ρ of this build. */
-#define FBS_MAX_RADIUS 6
+/* Maximum supported aggregation radius ρ of this build (FBS_PATH_VOLUME; the
+ * fused path supports ρ <= 6 and returns FBS_E_UNSUPPORTED above). */
+#define FBS_MAX_RADIUS 10
 /* -log2 of the smallest accepted tap weight ω_d·ω_r (see fbs_create). */
 #define FBS_MAX_WEIGHT_EXP2 124
 

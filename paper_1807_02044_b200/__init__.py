@@ -21,7 +21,8 @@ FBS_OK = 0
 FBS_E_ARG, FBS_E_PARAM, FBS_E_DIM, FBS_E_UNSUPPORTED, FBS_E_CUDA, FBS_E_OOM = -1, -2, -3, -4, -5, -6
 FBS_INVALID = -1.0
 FBS_SENTINEL = -2.0
-FBS_MAX_RADIUS = 6
+FBS_MAX_RADIUS = 10  # volume path; the fused path stops at 6
+FBS_FUSED_MAX_RADIUS = 6
 FBS_PATH_VOLUME, FBS_PATH_FUSED = 0, 1
 PATHS = {"volume": FBS_PATH_VOLUME, "fused": FBS_PATH_FUSED}
 

@@ -243,8 +243,8 @@ static fbs_ctx* create_impl(int W, int H, int d_min, int d_max, int radius, floa
       return nullptr;
     }
   }
-  if (radius > kMaxRadius) {
-    fail(FBS_E_UNSUPPORTED, "fbs_create: radius > FBS_MAX_RADIUS");
+  if (radius > kMaxRadius || (path == FBS_PATH_FUSED && radius > kFusedMaxRadius)) {
+    fail(FBS_E_UNSUPPORTED, "fbs_create: radius > FBS_MAX_RADIUS (10; 6 on the fused path)");
     return nullptr;
   }
   if ((long long)d_max - d_min + 1 > 4096 || W > (1 << 20) || H > (1 << 20)) {
@@ -437,7 +437,7 @@ static fbs_ctx* create_volume(fbs_ctx* h) {
   cudaFuncSetAttribute(vol::k_agg<RR, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
                        sizeof(vol::AggSmem<RR>));
   FBS_SMEM_ATTR(0) FBS_SMEM_ATTR(1) FBS_SMEM_ATTR(2) FBS_SMEM_ATTR(3) FBS_SMEM_ATTR(4)
-  FBS_SMEM_ATTR(5) FBS_SMEM_ATTR(6)
+  FBS_SMEM_ATTR(5) FBS_SMEM_ATTR(6) FBS_SMEM_ATTR(7) FBS_SMEM_ATTR(8) FBS_SMEM_ATTR(9) FBS_SMEM_ATTR(10)
 #undef FBS_SMEM_ATTR
   cudaFuncSetAttribute(vol::k_cost, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)vol::cost_smem_bytes(4096 / kDB));
@@ -570,6 +570,7 @@ static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0,
                               sizeof(vol::AggSmem<RR>), s, a);                                                \
     break;
       FBS_CASE(0) FBS_CASE(1) FBS_CASE(2) FBS_CASE(3) FBS_CASE(4) FBS_CASE(5) FBS_CASE(6)
+      FBS_CASE(7) FBS_CASE(8) FBS_CASE(9) FBS_CASE(10)
 #undef FBS_CASE
     }
     if (e != cudaSuccess) return cuda_check(e, "k_agg launch");

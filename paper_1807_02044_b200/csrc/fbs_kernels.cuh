@@ -38,7 +38,8 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 constexpr float kSent = -2.0f;   // undefined aggregated cost / exported cost (R#7)
 constexpr float kUndef = -0.0f;  // undefined cost in the cost ring (never a defined NCC value)
-constexpr int kMaxRadius = 6;    // FBS_MAX_RADIUS
+constexpr int kMaxRadius = 10;   // FBS_MAX_RADIUS (volume path)
+constexpr int kFusedMaxRadius = 6;  // the fused path's largest radius
 constexpr int kWsMaxRadius = 4;  // radii run by the warp-specialised walker (fbs_ws.cuh)
 // Smallest tap weight the handle accepts, as -log2 (FBS_MAX_WEIGHT_EXP2, R#13):
 // 2^-124 stays a normal fp32 after ex2.approx.ftz and any rounding of the exponent.

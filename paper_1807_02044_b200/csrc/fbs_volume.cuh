@@ -27,7 +27,7 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 constexpr float kSent = -2.0f;   // undefined aggregated cost / exported cost (R#7)
 constexpr float kUndef = -0.0f;  // undefined cost inside the volumes (never a defined NCC value)
-constexpr int kMaxRadius = 6;    // FBS_MAX_RADIUS
+constexpr int kMaxRadius = 10;   // FBS_MAX_RADIUS (volume path; the fused path stops at 6)
 constexpr int kDB = 64;          // disparities per block (32 lanes x 2)
 constexpr int kPX = 4;           // warp sub-tile width  (pixels)
 constexpr int kPYMax = 6;        // warp sub-tile height (pixels) for radius <= 5
@@ -37,18 +37,23 @@ constexpr int kTX = kPX * kNWX;  // CTA tile width (16)
 // Per-radius CTA geometry of k_agg: the weight buffers grow as (2ρ+1)², so the
 // largest radius uses one warp row (4 warps, 16x6 tiles) to keep several CTAs
 // resident per SM.
+// ρ >= 7 (NEXT-1, the paper's Fig. 7 range): one output row per half-warp, the
+// stream as a cost-row loop (the unrolled form would not fit the instruction
+// cache), two CTAs per SM up to ρ = 8 and one beyond (weights: 2 K1² x 4 px per warp).
 template <int R>
 struct AggGeom {
-  static constexpr int HPY = R >= 6 ? 2 : 3;      // output rows per half-warp
+  static constexpr int HPY = R >= 7 ? 1 : (R >= 6 ? 2 : 3);  // output rows per half-warp
   static constexpr int PY = 2 * HPY;              // warp sub-tile height (4 x PY pixels)
   static constexpr int NWY = 2;                   // warps down a CTA tile
   static constexpr int NW = kNWX * NWY;
   static constexpr int TY = PY * NWY;             // CTA tile height
   static constexpr int THREADS = 32 * NW;
-  static constexpr int MINB = 2;                  // CTAs per SM the registers are budgeted for
+  static constexpr int MINB = R >= 9 ? 1 : 2;     // CTAs per SM the registers are budgeted for
+  static constexpr bool kRolled = R >= 7;         // cost-row loop instead of the unrolled stream
+  static constexpr int CWS = R >= 7 ? 96 : 64;    // classification words per warp (PY + 2R <= 24 rows x 4)
 };
 constexpr int kTYMax = kPYMax * 2;                // tallest CTA tile of any radius
-__host__ __device__ constexpr int agg_tile_h(int R) { return (R >= 6 ? 4 : kPYMax) * 2; }
+__host__ __device__ constexpr int agg_tile_h(int R) { return R >= 7 ? 4 : (R >= 6 ? 4 : kPYMax) * 2; }
 
 #ifndef FBS_KCX
 #define FBS_KCX 64
@@ -370,7 +375,7 @@ struct AggSmem {
   float rinv[NW][32];                               // 1 / Σ_q w'(p,q), 0 if none
   float cs[NW][32][K1 + 1];                         // EDGE: 1 / suffix (left) or prefix (right) column sums
   float g[GH * GWS];                                // guide tile (padded image values, see kGuideFlag)
-  uint32_t cwb[NW][2][64];                          // classification words: current / next d-block
+  uint32_t cwb[NW][2][AggGeom<R>::CWS];             // classification words: current / next d-block
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -412,7 +417,7 @@ __device__ __forceinline__ void cw_load(const AggArgs& a, int side, int sx, int 
   const CwRange<R> g(a, side, sx, sy, b);
   const uint32_t* bits = side == 0 ? a.bitsR : a.bitsL;
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {  // slot i = 4 row + word (no division)
+  for (int k = 0; k < AggGeom<R>::CWS / 32; ++k) {  // slot i = 4 row + word (no division)
     const int i = lane + 32 * k, row = i >> 2, wd = i & 3;
     if (row < g.rows && wd < g.nw) cp_async4(cwb + i, bits + (size_t)(g.qy0 + row) * a.Wb + g.w0 + wd);
   }
@@ -423,7 +428,7 @@ __device__ __forceinline__ int cw_classify(const AggArgs& a, int side, int sx, i
   const CwRange<R> g(a, side, sx, sy, b);
   bool tex = false;
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < AggGeom<R>::CWS / 32; ++k) {
     const int i = lane + 32 * k, row = i >> 2, wd = i & 3;
     if (row < g.rows && wd < g.nw) {
       const int wi = g.w0 + wd;
@@ -448,7 +453,7 @@ __device__ __forceinline__ bool cw_empty(const AggArgs& a, int side, int sx, int
   const CwRange<R> g(a, side, sx, sy, b);
   bool def = false;
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < AggGeom<R>::CWS / 32; ++k) {
     const int i = lane + 32 * k, row = i >> 2, wd = i & 3;
     if (row < g.rows && wd < g.nw) {
       const int wi = g.w0 + wd;
@@ -547,6 +552,30 @@ __device__ __forceinline__ void agg_num4(const float* __restrict__ vb, size_t ro
   for (int py = 0; py < NPY; ++py)
 #pragma unroll
     for (int px = 0; px < kPX; ++px) num[py][px][0] = num[py][px][1] = make_float2(0.f, 0.f);
+  if constexpr (AggGeom<R>::kRolled) {
+    static_assert(NPY == 1, "the rolled stream feeds one output row per cost row");
+    constexpr int K1 = 2 * R + 1, NC = kPX + 2 * R;
+#pragma unroll 1
+    for (int r = 0; r < K1; ++r) {  // cost row r = window row dy (same order as the unrolled form)
+      const float* rp = vb + (size_t)r * rowstride;
+      float4 c[NC];
+#pragma unroll
+      for (int j = 0; j < NC; ++j) c[j] = __ldg(reinterpret_cast<const float4*>(rp + j * kDB));
+      const float* wr = wsm + r * K1 * kPX;
+#pragma unroll
+      for (int dx = 0; dx < K1; ++dx) {
+        const float4 w = reinterpret_cast<const float4*>(wr)[dx];
+        const float wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int px = 0; px < kPX; ++px) {
+          const float4 cc = c[dx + px];
+          ffma2(num[0][px][0], wv[px], make_float2(cc.x, cc.y));
+          ffma2(num[0][px][1], wv[px], make_float2(cc.z, cc.w));
+        }
+      }
+    }
+    return;
+  }
   float4 head[kPX];
 #pragma unroll
   for (int j = 0; j < kPX; ++j) head[j] = __ldg(reinterpret_cast<const float4*>(vb + j * kDB));
@@ -661,7 +690,8 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
     // the weight stores may alias the guide/LUT loads as far as ptxas can tell,
     // so interleaving them would serialise every LDS -> LDS -> STS chain.
     constexpr int CH = (K1 * K1 <= 64) ? K1 : (64 / K1 > 0 ? 64 / K1 : 1);
-#pragma unroll
+    constexpr int kChunkUnroll = AggGeom<R>::kRolled ? 1 : 16;  // ρ >= 7: chunks in a loop (code size)
+#pragma unroll kChunkUnroll
     for (int dy0 = 0; dy0 < K1; dy0 += CH) {
       constexpr int NB = CH * K1;
       float gv[NB];

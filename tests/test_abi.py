@@ -75,7 +75,7 @@ def test_sass_uses_ffma2_tma_dp4a():
     ((10, 10, 0, 5, -1, 1.0, 1.0), -2),
     ((10, 10, 0, 5, 1, 0.0, 1.0), -2),
     ((10, 10, 0, 5, 1, 1.0, float("nan")), -2),
-    ((10, 10, 0, 5, 7, 1.0, 1.0), -4),
+    ((10, 10, 0, 5, 11, 5.0, 40.0), -4),  # radius > FBS_MAX_RADIUS
     ((10, 10, 0, 5, 4, 5.0, 10.0), -4),   # smallest tap weight < 2^-124 (R#13)
     ((10, 10, 0, 5, 3, 0.7, 32.0), -4),
 ])

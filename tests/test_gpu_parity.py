@@ -124,8 +124,10 @@ def test_volumes_and_maps(fbs, oracle_lib, case, path):
     print(name, rep, "oracle near-tie pixels:", n_tie_ref)
 
 
-@pytest.mark.parametrize("path", PATHS)
-@pytest.mark.parametrize("rho", [0, 1, 2, 3, 4, 5, 6])
+RADII = [(r, p) for p in PATHS for r in range(0, 11) if p == "volume" or r <= 6]
+
+
+@pytest.mark.parametrize("rho,path", RADII, ids=[f"{r}-{p}" for r, p in RADII])
 def test_all_radii(fbs, oracle_lib, rho, path):
     W, H, d_min, d_max = 70, 36, 0, 23
     L, R = make_pair("layered", W, H, d_min, d_max, 40 + rho)
@@ -290,7 +292,7 @@ def test_tiny_frames(fbs, oracle_lib, path):
     worst = 0.0
     for t in range(40):
         W, H = int(rng.integers(3, 18)), int(rng.integers(3, 18))
-        rho = t % (fbs.FBS_MAX_RADIUS + 1)
+        rho = t % ((fbs.FBS_MAX_RADIUS if path == "volume" else fbs.FBS_FUSED_MAX_RADIUS) + 1)
         d_min = int(rng.integers(0, 4))
         d_max = d_min + int(rng.integers(1, W + 4))
         if t % 3 == 0:
