@@ -152,13 +152,13 @@ def load_traffic(cfgname, path):
         return None
 
 
-def bench_config(cfg, world):
+def bench_config(cfg, world, batch=1):
     """The `config` object of the JSON line — identical for both arms (the driver
     compares them): the workload, its partition across ranks and the inputs."""
     banded = cfg.name == "mb2014"
     return {"workload": f"{cfg.name} {cfg.W}x{cfg.H} d={cfg.d_min}..{cfg.d_max} (D={cfg.D}) "
                         f"rho={cfg.radius} gamma_d={cfg.gamma_d} gamma_r={cfg.gamma_r}",
-            "frames_per_step_per_rank": 1,
+            "frames_per_step_per_rank": batch,
             "partition": (f"row bands x{world} + NCCL all-gather" if banded else
                           f"frame sharding x{world}, no data-path collective"),
             "l2": "256 MiB L2 flush between timed steps (outside the step events)",
@@ -175,7 +175,9 @@ def run_ours(args, cfg, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     banded = cfg.name == "mb2014"
-    nfr = 1 if banded else 4
+    B = 1 if banded else args.batch  # frames per step (NEXT-2: fbs_compute_batch, one launch per <= 16 frames
+                                     # on the fused path)
+    nfr = 1 if banded else max(4, B)
     frames_np = [synth.frame(cfg, i + (0 if banded else 1000 * rank)) for i in range(nfr)]
     Ls = [torch.from_numpy(L).to(dev) for L, _ in frames_np]
     Rs = [torch.from_numpy(R).to(dev) for _, R in frames_np]
@@ -186,10 +188,17 @@ def run_ours(args, cfg, rank, world, local_rank):
     out = torch.empty((cfg.H, cfg.W), dtype=torch.float32, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
+    if B > 1:  # stacked batches, rotating through the frames
+        nb = 4
+        Lb = [torch.stack([Ls[(j * B + k) % nfr] for k in range(B)]) for j in range(nb)]
+        Rb = [torch.stack([Rs[(j * B + k) % nfr] for k in range(B)]) for j in range(nb)]
+        outb = torch.empty((B, cfg.H, cfg.W), dtype=torch.float32, device=dev)
 
     def step(i):
         L, R = Ls[i % nfr], Rs[i % nfr]
-        if banded:
+        if B > 1:
+            m.compute_batch(Lb[i % nb], Rb[i % nb], out=outb)
+        elif banded:
             fdist.compute_banded(lambda r0, r1, band: m.compute_rows(L, R, r0, r1, out=band[: r1 - r0]),
                                  cfg.H, cfg.W, rank, world, device=dev)
         else:
@@ -206,19 +215,22 @@ def run_ours(args, cfg, rank, world, local_rank):
         cs = torch.cuda.Stream()
         cs.wait_stream(stream)
         with torch.cuda.stream(cs):
-            for i in range(nfr):
+            for i in range(nfr if B == 1 else nb):
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=cs):
-                    m.compute(Ls[i], Rs[i], out=out, stream=cs)
+                    if B == 1:
+                        m.compute(Ls[i], Rs[i], out=out, stream=cs)
+                    else:
+                        m.compute_batch(Lb[i], Rb[i], out=outb, stream=cs)
                 graphs.append(g)
         torch.cuda.synchronize()
         for i in range(args.warmup):
-            graphs[i % nfr].replay()
+            graphs[i % len(graphs)].replay()
         torch.cuda.synchronize()
 
     def timed_step(i):
         if graphs:
-            graphs[i % nfr].replay()
+            graphs[i % len(graphs)].replay()
         else:
             step(i)
 
@@ -244,7 +256,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     # region (stage events between the launches would serialise the programmatic
     # dependent launches, so they stay out of the timed steps)
     nprof_steps = min(args.steps, 500)
-    m.profile_enable(nprof_steps)
+    m.profile_enable(nprof_steps * B)  # events per launch sequence: per frame (volume) or per batch (fused)
     for i in range(nprof_steps):
         flush.fill_(float(i))
         step(i)
@@ -256,7 +268,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
-    frames_total = args.steps * (1 if banded else world)
+    frames_total = args.steps * (1 if banded else world * B)
     value = mdisp(cfg, frames_total, max_ms / 1e3)
 
     # ---- end to end through the public C ABI with pinned host buffers ----
@@ -314,7 +326,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         frac_rows = (rows[1] - rows[0]) / cfg.H
     else:
         frac_rows = 1.0
-    achieved = 2 * useful_flops_per_side(cfg) * frac_rows / (agg_ms * 1e-3) / 1e12
+    fpe = nprof_steps * B / max(1, nprof)  # frames per profiled launch (fused batches: up to 16)
+    achieved = 2 * useful_flops_per_side(cfg) * frac_rows * fpe / (agg_ms * 1e-3) / 1e12
     tot_stage = sum(stage_ms.values())
     roof = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "traffic": load_traffic(cfg.name, args.path),
@@ -326,8 +339,9 @@ def run_ours(args, cfg, rank, world, local_rank):
                       "launch, in a profiled pass of the same workload right after the timed steps",
             "share_of_step": round(stage_ms["main"] / tot_stage, 3) if tot_stage else None,
             "stage_ms_per_frame": {(("cost", "agg", "finalize") if args.path == "volume" else
-                                    ("prep", "fbs", "final"))[i]: round(v / max(1, nprof), 5)
+                                    ("prep", "fbs", "final"))[i]: round(v / max(1, nprof) / fpe, 5)
                                    for i, v in enumerate(stage_ms.values())},
+            "frames_per_launch": fpe,
             "peak_source": f"148 SM x 128 FP32 lanes x 2 x {peak_src} (nominal); "
                            "FFMA2 microbenchmark 66.9 TFLOP/s (DESIGN.md §6)",
             "useful_work": "numerator FMAs of Eq.(6): 2 sides x W*H*D*(2rho+1)^2 per launch",
@@ -350,7 +364,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (seeded layered Middlebury-like pairs, stereo_synth v%d)" % synth.SYNTH_VERSION,
-        "config": bench_config(cfg, world),
+        "config": bench_config(cfg, world, B),
         "path": args.path,
         "timing": ("CUDA-graph replay of fbs_compute per step" if graphs else "eager launches per step"),
         "roofline": roof,
@@ -419,6 +433,8 @@ def main():
                     help="frames per end-to-end step (fbs_compute_host_batch pipeline depth)")
     ap.add_argument("--radius", type=int, default=None,
                     help="override the config's aggregation radius rho (NEXT-1 sweep; paper's operating point is 6)")
+    ap.add_argument("--batch", type=int, default=1,
+                    help="frames per step through fbs_compute_batch (NEXT-2; not for mb2014)")
     ap.add_argument("--no-graph", action="store_true",
                     help="time eager launches instead of CUDA-graph replays")
     ap.add_argument("--no-extras", action="store_true",
