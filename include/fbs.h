@@ -251,6 +251,29 @@ int fbs_profile_read(fbs_ctx* h, double* stage_ms, int* ncalls);
  */
 int fbs_tile_stats(fbs_ctx* h, long long* fast, long long* edge, long long* general, long long* empty);
 
+/*
+ * Disparity-range split (NEXT-3): rank k computes the WTA over its
+ * own sub-range of disparities, the ranks reduce per-pixel 64-bit keys with MAX
+ * (NCCL all_reduce), then one call applies LRC + subpixel.
+ *
+ * fbs_compute_keys — volume-path handles only (else FBS_E_UNSUPPORTED).  Only the
+ * disparities [c_lo, c_hi] ⊆ [d_min, d_max] of the handle compete in the WTA; create
+ * the handle with one disparity beyond each end of [c_lo, c_hi] (clipped to the
+ * global range) so the subpixel neighbours exist.  Outputs (device, [H][W]):
+ *   keys_l, keys_r  uint64: (order-preserving bits of c_agg(p, d*)) << 32 | (0xFFFFFFFF - d*),
+ *                   d* the global disparity; MAX over keys = highest aggregated cost,
+ *                   smallest d on ties; 0 = no defined cost.
+ *   rec_l           float4 per pixel: (c(d*-1), c(d*), c(d*+1), 0) of the left volume,
+ *                   FBS_SENTINEL where undefined or outside the handle's range.
+ * fbs_finalize_keys — LRC (Eq.(9)) + subpixel (Eq.(10)) of the global range
+ * [d_min, d_max] from the reduced keys and the winners' records -> disp_out
+ * (device float [H][W]).  No handle needed.  Both asynchronous on `stream`.
+ */
+int fbs_compute_keys(fbs_ctx* h, const uint8_t* left, const uint8_t* right, int c_lo, int c_hi,
+                     uint64_t* keys_l, uint64_t* keys_r, float* rec_l, fbs_stream_t stream);
+int fbs_finalize_keys(int W, int H, int d_min, int d_max, const uint64_t* keys_l, const uint64_t* keys_r,
+                      const float* rec_l, float* disp_out, fbs_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,7 +27,7 @@ FBS_PATH_VOLUME, FBS_PATH_FUSED = 0, 1
 PATHS = {"volume": FBS_PATH_VOLUME, "fused": FBS_PATH_FUSED}
 
 # every symbol include/fbs.h declares
-EXPORTS = ("fbs_create", "fbs_create_ex", "fbs_create_band", "fbs_destroy", "fbs_last_error", "fbs_compute", "fbs_compute_rows",
+EXPORTS = ("fbs_create", "fbs_create_ex", "fbs_create_band", "fbs_compute_keys", "fbs_finalize_keys", "fbs_destroy", "fbs_last_error", "fbs_compute", "fbs_compute_rows",
            "fbs_compute_batch", "fbs_compute_host", "fbs_compute_host_batch", "fbs_debug_volumes", "fbs_debug_select",
            "fbs_debug_maps", "fbs_stats", "fbs_profile_enable", "fbs_profile_read", "fbs_tile_stats")
 FBS_NSTAGES = 3
@@ -57,6 +57,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.fbs_create_ex.restype = P
     lib.fbs_create_band.argtypes = [I, I, I, I, I, F, F, I, I, I]
     lib.fbs_create_band.restype = P
+    lib.fbs_compute_keys.argtypes = [P, P, P, I, I, P, P, P, P]
+    lib.fbs_compute_keys.restype = I
+    lib.fbs_finalize_keys.argtypes = [I, I, I, I, P, P, P, P, P]
+    lib.fbs_finalize_keys.restype = I
     lib.fbs_destroy.argtypes = [P]
     lib.fbs_destroy.restype = None
     lib.fbs_last_error.argtypes = []
@@ -127,6 +131,30 @@ def fbs_create_band(W: int, H: int, d_min: int, d_max: int, radius: int, sigma_s
     if not h:
         raise FbsError(FBS_E_PARAM, last_error())
     return ctypes.c_void_p(h)
+
+
+def fbs_compute_keys(h, left, right, c_lo: int, c_hi: int, keys_l, keys_r, rec_l, stream=None) -> None:
+    _check(load_library().fbs_compute_keys(h, _ptr(left), _ptr(right), c_lo, c_hi, _ptr(keys_l), _ptr(keys_r),
+                                           _ptr(rec_l), _stream(stream)))
+
+
+def fbs_finalize_keys(W: int, H: int, d_min: int, d_max: int, keys_l, keys_r, rec_l, disp_out,
+                      stream=None) -> None:
+    _check(load_library().fbs_finalize_keys(W, H, d_min, d_max, _ptr(keys_l), _ptr(keys_r), _ptr(rec_l),
+                                            _ptr(disp_out), _stream(stream)))
+
+
+def finalize_keys(W: int, H: int, d_min: int, d_max: int, keys_l, keys_r, rec_l, out=None, stream=None):
+    """LRC + subpixel from reduced keys (int64 [H, W] holding the uint64 bits) and
+    records (float32 [H, W, 4]) on their device."""
+    import torch
+    for t, dt, shp in ((keys_l, torch.int64, (H, W)), (keys_r, torch.int64, (H, W)), (rec_l, torch.float32, (H, W, 4))):
+        if t.dtype != dt or tuple(t.shape) != shp or not t.is_cuda or not t.is_contiguous():
+            raise ValueError(f"finalize_keys: expected contiguous {dt} {shp} device tensors")
+    if out is None:
+        out = torch.empty((H, W), dtype=torch.float32, device=keys_l.device)
+    fbs_finalize_keys(W, H, d_min, d_max, keys_l, keys_r, rec_l, out, stream)
+    return out
 
 
 def fbs_destroy(h) -> None:
@@ -322,6 +350,18 @@ class FBS:
         dr = torch.empty_like(dl)
         fbs_debug_maps(self.h, left, right, out, dl, dr, stream)
         return out, dl, dr
+
+    def compute_keys(self, left, right, c_lo: int, c_hi: int, stream=None):
+        """Disparity-range split (volume path): the WTA over [c_lo, c_hi] only.
+        Returns keys_l, keys_r (int64 [H, W] holding the uint64 keys) and rec_l
+        (float32 [H, W, 4]: c(d*-1), c(d*), c(d*+1), 0)."""
+        import torch
+        self._chk_pair(left, right)
+        kl = torch.empty((self.H, self.W), dtype=torch.int64, device=self.device)
+        kr = torch.empty_like(kl)
+        rec = torch.empty((self.H, self.W, 4), dtype=torch.float32, device=self.device)
+        fbs_compute_keys(self.h, left, right, c_lo, c_hi, kl, kr, rec, stream)
+        return kl, kr, rec
 
     def select(self, agg_l, agg_r, stream=None):
         import torch

@@ -435,6 +435,8 @@ static fbs_ctx* create_volume(fbs_ctx* h) {
   cudaFuncSetAttribute(vol::k_agg<RR, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,             \
                        sizeof(vol::AggSmem<RR>));                                                             \
   cudaFuncSetAttribute(vol::k_agg<RR, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
+                       sizeof(vol::AggSmem<RR>));                                                             \
+  cudaFuncSetAttribute(vol::k_agg<RR, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
                        sizeof(vol::AggSmem<RR>));
   FBS_SMEM_ATTR(0) FBS_SMEM_ATTR(1) FBS_SMEM_ATTR(2) FBS_SMEM_ATTR(3) FBS_SMEM_ATTR(4)
   FBS_SMEM_ATTR(5) FBS_SMEM_ATTR(6) FBS_SMEM_ATTR(7) FBS_SMEM_ATTR(8) FBS_SMEM_ATTR(9) FBS_SMEM_ATTR(10)
@@ -506,9 +508,17 @@ static cudaError_t launch_walk(const fbs_ctx* h, const WalkArgs& a, bool exp, cu
   return cudaErrorInvalidValue;
 }
 
+// Disparity-range split request (fbs_compute_keys): competing range [c_lo, c_hi]
+// (handle-local indices) and the outputs replacing the final map.
+struct KeysReq {
+  int c_lo, c_hi;
+  unsigned long long *keys_l, *keys_r;
+  float4* rec_l;
+};
+
 // Volume path, one frame: output rows [r0, r1); exports when expC/expA are set.
 static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0, int r1, float* out,
-                      float* const* expC, float* const* expA, cudaStream_t s) {
+                      float* const* expC, float* const* expA, cudaStream_t s, const KeysReq* kq = nullptr) {
   const int W = h->W, H = h->H, R = h->R;
   // aggregation tiles are anchored at multiples of the tile height in frame rows, so a
   // pixel's denominator form never depends on the band; cost rows cover the
@@ -558,6 +568,10 @@ static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0,
   }
   a.agg3 = (h->nblk == 1 && !aggL_exp) ? h->agg3 : nullptr;
   a.tile_stats = ev ? h->tile_stats : nullptr;
+  a.c_lo = kq ? kq->c_lo : 0;
+  a.c_hi = kq ? kq->c_hi : h->D - 1;
+  a.keys_out[0] = kq ? kq->keys_l : nullptr;
+  a.keys_out[1] = kq ? kq->keys_r : nullptr;
   {
     const dim3 grid((W + vol::kTX - 1) / vol::kTX, ty1 - ty0, 2);
     cudaError_t e = cudaErrorInvalidValue;
@@ -565,6 +579,8 @@ static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0,
 #define FBS_CASE(RR)                                                                                          \
   case RR:                                                                                                    \
     e = aggR_exp ? launch_pdl(vol::k_agg<RR, false, true>, grid, dim3(vol::AggGeom<RR>::THREADS),             \
+                              sizeof(vol::AggSmem<RR>), s, a)                                                 \
+        : kq     ? launch_pdl(vol::k_agg<RR, false, false, true>, grid, dim3(vol::AggGeom<RR>::THREADS),      \
                               sizeof(vol::AggSmem<RR>), s, a)                                                 \
                  : launch_pdl(vol::k_agg<RR, false, false>, grid, dim3(vol::AggGeom<RR>::THREADS),            \
                               sizeof(vol::AggSmem<RR>), s, a);                                                \
@@ -577,6 +593,14 @@ static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0,
     h->launches += 1;
   }
   if (ev) cudaEventRecord(ev[2], s);
+  if (kq) {  // disparity-range split: the records instead of the final map
+    const dim3 grd((W + 127) / 128, r1 - r0);
+    vol::k_records<<<grd, 128, 0, s>>>(h->dmap[0], a.aggL, a.agg3, h->nblk, W, r0, r1, h->d_min, h->d_max, a.abase,
+                                       kq->rec_l);
+    h->launches += 1;
+    if (ev) cudaEventRecord(ev[3], s);
+    return cuda_check(cudaGetLastError(), "fbs_compute_keys launch");
+  }
   {
     const dim3 grd((W + 127) / 128, r1 - r0);
     const cudaError_t e = launch_pdl(vol::k_finalize, grd, dim3(128), 0, s, (const int32_t*)h->dmap[0],
@@ -872,3 +896,28 @@ extern "C" int fbs_debug_trace(fbs_ctx* h, unsigned long long* host, int n) {
   return cuda_check(cudaMemcpy(host, h->trace, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "trace");
 }
 #endif
+
+// ---------------------------------------------------------------------------
+// Disparity-range split (NEXT-3, SURVEY §8(e) "Alternative").
+extern "C" int fbs_compute_keys(fbs_ctx* h, const uint8_t* left, const uint8_t* right, int c_lo, int c_hi,
+                                uint64_t* keys_l, uint64_t* keys_r, float* rec_l, fbs_stream_t stream) {
+  if (!h || !left || !right || !keys_l || !keys_r || !rec_l) return fail(FBS_E_ARG, "fbs_compute_keys: NULL argument");
+  if (h->path != FBS_PATH_VOLUME) return fail(FBS_E_UNSUPPORTED, "fbs_compute_keys: volume path only");
+  if (!full_frame(h)) return fail(FBS_E_ARG, "fbs_compute_keys: band handle");
+  if (c_lo < h->d_min || c_hi > h->d_max || c_lo > c_hi)
+    return fail(FBS_E_ARG, "fbs_compute_keys: need d_min <= c_lo <= c_hi <= d_max (the handle's range)");
+  KeysReq kq{c_lo - h->d_min, c_hi - h->d_min, (unsigned long long*)keys_l, (unsigned long long*)keys_r,
+             (float4*)rec_l};
+  return run_volume(h, left, right, 0, h->H, nullptr, nullptr, nullptr, (cudaStream_t)stream, &kq);
+}
+
+extern "C" int fbs_finalize_keys(int W, int H, int d_min, int d_max, const uint64_t* keys_l, const uint64_t* keys_r,
+                                 const float* rec_l, float* disp_out, fbs_stream_t stream) {
+  if (!keys_l || !keys_r || !rec_l || !disp_out) return fail(FBS_E_ARG, "fbs_finalize_keys: NULL argument");
+  if (W < 3 || H < 3 || d_min < 0 || d_max <= d_min) return fail(FBS_E_PARAM, "fbs_finalize_keys: bad geometry");
+  const dim3 grd((W + 127) / 128, H);
+  vol::k_finalize_keys<<<grd, 128, 0, (cudaStream_t)stream>>>((const unsigned long long*)keys_l,
+                                                              (const unsigned long long*)keys_r,
+                                                              (const float4*)rec_l, W, H, d_min, d_max, disp_out);
+  return cuda_check(cudaGetLastError(), "fbs_finalize_keys");
+}

@@ -296,6 +296,56 @@ __global__ void k_finalize(const int32_t* __restrict__ dl, const int32_t* __rest
   out[(size_t)(y - r0) * W + x] = finalize_pixel(d, e, c0, cm, cp, d_min, d_max);
 }
 
+// KEYS: the left record (c(d*-1), c(d*), c(d*+1)) of every pixel of rows [r0, r1)
+// for the disparity-range split (same sources and rules as k_finalize; the
+// neighbours come from the handle's whole range, which includes one disparity
+// beyond each end of the competing range).
+__global__ void k_records(const int32_t* __restrict__ dl, const float* __restrict__ aggL,
+                          const float4* __restrict__ agg3, int nblk, int W, int r0, int r1, int d_min, int d_max,
+                          int abase, float4* __restrict__ rec) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = r0 + blockIdx.y;
+  if (x >= W || y >= r1) return;
+  const size_t p = (size_t)y * W + x;
+  const int d = dl[p];
+  float c0 = kSent, cm = kSent, cp = kSent;
+  if (d >= 0 && agg3) {
+    const float4 v = agg3[p];
+    cm = v.x; c0 = v.y; cp = v.z;
+  } else if (d >= 0) {
+    auto at = [&](int di) { return aggL[(((size_t)(y - abase) * nblk + di / kDB) * W + x) * kDB + di % kDB]; };
+    const int di = d - d_min;
+    c0 = at(di);
+    if (d > d_min) cm = at(di - 1);
+    if (d < d_max) cp = at(di + 1);
+  }
+  rec[p] = make_float4(cm, c0, cp, 0.f);
+}
+
+// LRC + subpixel from (reduced) keys and records: the disparity-range split's last
+// step; identical rules to k_finalize on the global range [d_min, d_max].
+__global__ void k_finalize_keys(const unsigned long long* __restrict__ kl, const unsigned long long* __restrict__ kr,
+                                const float4* __restrict__ rec, int W, int H, int d_min, int d_max,
+                                float* __restrict__ out) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y;
+  if (x >= W || y >= H) return;
+  const size_t p = (size_t)y * W + x;
+  const unsigned long long k = kl[p];
+  const int d = k ? (int)(0xffffffffu - (unsigned)(k & 0xffffffffu)) : -1;
+  int e = -1;
+  if (d >= 0 && x - d >= 0) {
+    const unsigned long long ke = kr[p - d];
+    e = ke ? (int)(0xffffffffu - (unsigned)(ke & 0xffffffffu)) : -1;
+  }
+  float c0 = kSent, cm = kSent, cp = kSent;
+  if (d >= 0) {
+    const float4 v = rec[p];
+    cm = v.x; c0 = v.y; cp = v.z;
+  }
+  out[p] = finalize_pixel(d, e, c0, cm, cp, d_min, d_max);
+}
+
 // left aggregated store -> [H][W][D] export (debug)
 __global__ void k_export_agg(const float* __restrict__ aggL, int W, int H, int D, int nblk,
                              float* __restrict__ out) {
@@ -338,6 +388,10 @@ struct AggArgs {
   float4* agg3;                  // if set (one d-block, no export): only (c(d*-1), c(d*), c(d*+1)) per
                                  // left pixel, [H][W] float4, instead of aggL
   float* exportR;                // optional [H][W][D] right aggregated volume (debug)
+  // KEYS instantiation (disparity-range split, NEXT-3): only local disparity indices
+  // [c_lo, c_hi] compete in the WTA; the per-pixel keys (global d) are written out
+  int c_lo, c_hi;
+  unsigned long long* keys_out[2];
   unsigned long long* tile_stats;  // optional [4]: FAST / EDGE / GENERAL / EMPTY (sub-tile, d-block) counts
   float cd[(2 * kMaxRadius + 1) * (2 * kMaxRadius + 1)];  // log2 ω_d = -log2(e)(dx²+dy²)/γ_d², Eq.(7)
   float nkr;                                               // -log2(e)/γ_r²: log2 ω_r = nkr Δ², Eq.(8)
@@ -642,7 +696,7 @@ __device__ __forceinline__ unsigned long long wta_butterfly16(unsigned long long
 // between both bodies compiled 20 % slower still).  Bit-identical results.
 // EXPORT: the debug export of the right aggregated volume is compiled in (its
 // store loop alone costs the production kernel ~1 %).
-template <int R, bool EMPTY, bool EXPORT>
+template <int R, bool EMPTY, bool EXPORT, bool KEYS = false>
 __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(const AggArgs a) {
   constexpr int kPY = AggGeom<R>::PY;
   constexpr int kTY = AggGeom<R>::TY;
@@ -772,15 +826,21 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
     for (int s2 = kPX * HPY; s2 < 16; ++s2) k[s2] = 0ull;
     const int di0 = b * kDB + 4 * dq;
     // padded disparity slots of the last block never win: their values get -inf
-    float pad[4];
+    float pad[4], cpad[4];  // cpad (KEYS): disparities outside [c_lo, c_hi] do not compete
 #pragma unroll
-    for (int t = 0; t < 4; ++t) pad[t] = di0 + t < a.D ? 0.f : -INFINITY;
+    for (int t = 0; t < 4; ++t) {
+      pad[t] = di0 + t < a.D ? 0.f : -INFINITY;
+      cpad[t] = KEYS ? (di0 + t >= a.c_lo && di0 + t <= a.c_hi ? 0.f : -INFINITY) : 0.f;
+    }
     // aggregated costs (d = di0 .. di0+3) of half-row pixel (pyl, px) -> key, left store, export
     // (FAST / EDGE pass the padded values themselves, PADDED = true)
     auto emit = [&](int pyl, int px, float4 agg, bool padded) {
       const int y = sy + py0 + pyl, x = sx + px;
-      const float v0 = padded ? agg.x : agg.x + pad[0], v1 = padded ? agg.y : agg.y + pad[1],
-                  v2 = padded ? agg.z : agg.z + pad[2], v3 = padded ? agg.w : agg.w + pad[3];
+      float v0 = padded ? agg.x : agg.x + pad[0], v1 = padded ? agg.y : agg.y + pad[1],
+            v2 = padded ? agg.z : agg.z + pad[2], v3 = padded ? agg.w : agg.w + pad[3];
+      if constexpr (KEYS) {
+        v0 += cpad[0]; v1 += cpad[1]; v2 += cpad[2]; v3 += cpad[3];
+      }
       const bool h01 = v1 > v0, h23 = v3 > v2;     // equal values keep the smaller d
       const float b01 = h01 ? v1 : v0, b23 = h23 ? v3 : v2;
       const bool h = b23 > b01;
@@ -887,6 +947,9 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
         const bool ok = (unsigned)(best >> 32) > fkey(kSent);
         const int d_int = ok ? a.d_min + (0xffff - (int)(best & 0xffffu)) : -1;
         (side == 0 ? a.dL : a.dR)[(size_t)y * a.W + x] = d_int;
+        if constexpr (KEYS)  // global-d key: (value bits << 32) | (0xFFFFFFFF - d); 0 = no defined cost
+          a.keys_out[side][(size_t)y * a.W + x] =
+              ok ? ((best >> 32) << 32) | (unsigned long long)(0xffffffffu - (unsigned)d_int) : 0ull;
         if (side == 0 && a.agg3 && ok) {  // the three costs Eq.(10) needs
           const float* vr = vrow(s2 / kPX) + (s2 % kPX) * kDB;
           const int di = d_int - a.d_min;

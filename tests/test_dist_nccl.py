@@ -65,3 +65,42 @@ def test_nccl_bands_bit_identical(cfgname, path):
     mp.spawn(_worker, args=(world, _free_port(), cfgname, path, q), nprocs=world, join=True)
     got = q.get(timeout=60)
     assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+
+
+def _drange_worker(rank, world, port, q):
+    import torch.distributed as dist
+    import stereo_synth as synth
+    import paper_1807_02044_b200 as fbs
+    from paper_1807_02044_b200 import dist as fdist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    cfg = synth.CONFIGS["kitti"]
+    L, R = (torch.from_numpy(x).cuda() for x in synth.frame(cfg, 0))
+    out = fdist.compute_drange_split(
+        lambda a, b: fbs.FBS(cfg.W, cfg.H, a, b, cfg.radius, cfg.gamma_d, cfg.gamma_r),
+        L, R, cfg.W, cfg.H, cfg.d_min, cfg.d_max, rank, world)
+    if rank == 0:
+        q.put(out.cpu().numpy().copy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_nccl_drange_split():
+    """NEXT-3 over NCCL: the disparity-range split of a KITTI frame across the GPUs
+    gives the single-GPU map (near-tie pixels aside)."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs for an NCCL process group")
+    import torch.multiprocessing as mp
+    import stereo_synth as synth
+    import paper_1807_02044_b200 as fbs
+    world = min(8, torch.cuda.device_count())
+    cfg = synth.CONFIGS["kitti"]
+    L, R = (torch.from_numpy(x).cuda() for x in synth.frame(cfg, 0))
+    ref = fbs.FBS(cfg.W, cfg.H, cfg.d_min, cfg.d_max, cfg.radius, cfg.gamma_d, cfg.gamma_r).compute(L, R).cpu().numpy()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.spawn(_drange_worker, args=(world, _free_port(), q), nprocs=world, join=True)
+    got = q.get(timeout=60)
+    assert np.mean(got.view(np.uint32) == ref.view(np.uint32)) > 0.995

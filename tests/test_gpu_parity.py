@@ -385,3 +385,38 @@ def test_band_handles(fbs, path):
             # volumes + left store cover the band, not the frame (2 x 375-row volumes ~ 0.9 GB)
             assert used < 0.6e9, used
         m.close()
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_drange_split_matches_oracle(fbs, oracle_lib, world):
+    """NEXT-3, disparity-range split: `world` sub-range handles (simulated ranks on
+    one GPU), keys reduced by the same MAX arithmetic the NCCL all_reduce applies,
+    then LRC + subpixel from the keys -> the parity contract against the oracle,
+    and the same maps as the single full-range handle (near-ties aside)."""
+    from paper_1807_02044_b200 import dist as fdist
+    W, H, d_min, d_max, rho = 160, 96, 3, 100, 4
+    L, R = make_pair("half", W, H, d_min, d_max, 61 + world)
+    ref = oracle_lib.fbs(L, R, d_min, d_max, rho, 5.0, 32.0)
+    Ld, Rd = to_dev(L), to_dev(R)
+    keys_l, keys_r, recs = [], [], []
+    for lo, hi in fdist.drange_split(d_min, d_max, world):
+        a, b = fdist.handle_range(d_min, d_max, lo, hi)
+        m = fbs.FBS(W, H, a, b, rho, 5.0, 32.0)
+        kl, kr, rec = m.compute_keys(Ld, Rd, lo, hi)
+        keys_l.append(kl); keys_r.append(kr); recs.append(rec)
+    kl, rec = fdist.reduce_keys_local(keys_l, recs)
+    kr, _ = fdist.reduce_keys_local(keys_r, recs)
+    out = fbs.finalize_keys(W, H, d_min, d_max, kl, kr, rec.contiguous()).cpu().numpy()
+
+    def decode(k):
+        k = k.cpu().numpy().view(np.uint64)
+        return np.where(k == 0, -1, (np.uint64(0xFFFFFFFF) - (k & np.uint64(0xFFFFFFFF))).astype(np.int64))
+    dl, dr = decode(kl), decode(kr)
+    D = d_max - d_min + 1
+    rep = parity.MapReport()
+    parity.check_int_map(dl, ref.disp_l, lambda i, d: ref.agg_l.reshape(-1, D)[i, d - d_min], "d_L", rep)
+    parity.check_int_map(dr, ref.disp_r, lambda i, d: ref.agg_r.reshape(-1, D)[i, d - d_min], "d_R", rep)
+    parity.check_final(out, ref.disp, dl, ref.disp_l, dr, ref.disp_r, ref.sub_den, W, rep)
+    full, fdl, _ = (t.cpu().numpy() for t in fbs.FBS(W, H, d_min, d_max, rho, 5.0, 32.0).maps(Ld, Rd))
+    assert np.mean(fdl == dl) > 0.99
+    log_errors(f"drange-split-{world}", subpix=rep.max_subpix_err, near_ties=rep.near_ties, pixels=W * H)
