@@ -194,9 +194,16 @@ def run_ours(args, cfg, rank, world, local_rank):
         Rb = [torch.stack([Rs[(j * B + k) % nfr] for k in range(B)]) for j in range(nb)]
         outb = torch.empty((B, cfg.H, cfg.W), dtype=torch.float32, device=dev)
 
+    if args.sparse_margin is not None:  # NEXT-4: seeds = the full-range maps (a stream's previous frames)
+        seeds = [m.compute(Ls[i], Rs[i]) for i in range(nfr)] if world == 1 else None
+        torch.cuda.synchronize()
+
     def step(i):
         L, R = Ls[i % nfr], Rs[i % nfr]
-        if B > 1:
+        if args.sparse_margin is not None and world == 1:
+            rl, rr = m.suggest_ranges(seeds[i % nfr], args.sparse_margin)
+            m.compute_ranged(L, R, rl, rr, out=out)
+        elif B > 1:
             m.compute_batch(Lb[i % nb], Rb[i % nb], out=outb)
         elif banded:
             fdist.compute_banded(lambda r0, r1, band: m.compute_rows(L, R, r0, r1, out=band[: r1 - r0]),
@@ -211,7 +218,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     # the timed steps replay CUDA graphs of fbs_compute (one per input frame; SURVEY
     # §8(d)): fbs_compute only enqueues, so it captures as is
     graphs = []
-    if not banded and not args.no_graph:
+    if not banded and not args.no_graph and args.sparse_margin is None:
         cs = torch.cuda.Stream()
         cs.wait_stream(stream)
         with torch.cuda.stream(cs):
@@ -366,6 +373,9 @@ def run_ours(args, cfg, rank, world, local_rank):
         "data": "synthetic (seeded layered Middlebury-like pairs, stereo_synth v%d)" % synth.SYNTH_VERSION,
         "config": bench_config(cfg, world, B),
         "path": args.path,
+        "mode": (f"sparse search range (NEXT-4): per step fbs_suggest_ranges(margin={args.sparse_margin}) from "
+                 "the frame's full-range map + fbs_compute_ranged" if args.sparse_margin is not None
+                 else "full search range"),
         "timing": ("CUDA-graph replay of fbs_compute per step" if graphs else "eager launches per step"),
         "roofline": roof,
         "cpu_baseline": base,
@@ -435,6 +445,9 @@ def main():
                     help="override the config's aggregation radius rho (NEXT-1 sweep; paper's operating point is 6)")
     ap.add_argument("--batch", type=int, default=1,
                     help="frames per step through fbs_compute_batch (NEXT-2; not for mb2014)")
+    ap.add_argument("--sparse-margin", type=int, default=None,
+                    help="NEXT-4: per step, suggest ranges (margin M) from the frame's full-range map "
+                         "and run the ranged WTA (sparse search range)")
     ap.add_argument("--no-graph", action="store_true",
                     help="time eager launches instead of CUDA-graph replays")
     ap.add_argument("--no-extras", action="store_true",

@@ -274,6 +274,29 @@ int fbs_compute_keys(fbs_ctx* h, const uint8_t* left, const uint8_t* right, int 
 int fbs_finalize_keys(int W, int H, int d_min, int d_max, const uint64_t* keys_l, const uint64_t* keys_r,
                       const float* rec_l, float* disp_out, fbs_stream_t stream);
 
+/*
+ * Sparse search range (NEXT-4; the paper's future work; readings R#31-R#33
+ * in DESIGN.md).  Volume-path handles only (else FBS_E_UNSUPPORTED).
+ *
+ * fbs_suggest_ranges — per-pixel suggested ranges from "reliable feature points":
+ *   seed_disp  device float [H][W]: a disparity map whose values >= 0 are the
+ *              feature points (e.g. the previous frame's fbs_compute output)
+ *   margin     disparities added on each side (>= 0)
+ *   ranges_l, ranges_r  device int16 [H][W][2] out: (lo, hi) per pixel of the left
+ *              / right image = [floor(min) - margin, ceil(max) + margin] of the seeds
+ *              of its frame-anchored 16x16 tile (left seeds forward-warped to
+ *              x - round(s) for the right image), clipped to [d_min, d_max]; tiles
+ *              without a seed get [d_min, d_max].
+ * fbs_compute_ranged — fbs_compute with the WTA of each pixel restricted to its
+ *   range (ranges_* as above; lo > hi = no candidate); d-blocks outside the union
+ *   of a tile's ranges are not aggregated at all.  Subpixel only when d*±1 lie in
+ *   the pixel's range.  Both asynchronous on `stream`.
+ */
+int fbs_suggest_ranges(fbs_ctx* h, const float* seed_disp, int margin, int16_t* ranges_l, int16_t* ranges_r,
+                       fbs_stream_t stream);
+int fbs_compute_ranged(fbs_ctx* h, const uint8_t* left, const uint8_t* right, const int16_t* ranges_l,
+                       const int16_t* ranges_r, float* disp_out, fbs_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,7 +27,7 @@ FBS_PATH_VOLUME, FBS_PATH_FUSED = 0, 1
 PATHS = {"volume": FBS_PATH_VOLUME, "fused": FBS_PATH_FUSED}
 
 # every symbol include/fbs.h declares
-EXPORTS = ("fbs_create", "fbs_create_ex", "fbs_create_band", "fbs_compute_keys", "fbs_finalize_keys", "fbs_destroy", "fbs_last_error", "fbs_compute", "fbs_compute_rows",
+EXPORTS = ("fbs_create", "fbs_create_ex", "fbs_create_band", "fbs_compute_keys", "fbs_finalize_keys", "fbs_suggest_ranges", "fbs_compute_ranged", "fbs_destroy", "fbs_last_error", "fbs_compute", "fbs_compute_rows",
            "fbs_compute_batch", "fbs_compute_host", "fbs_compute_host_batch", "fbs_debug_volumes", "fbs_debug_select",
            "fbs_debug_maps", "fbs_stats", "fbs_profile_enable", "fbs_profile_read", "fbs_tile_stats")
 FBS_NSTAGES = 3
@@ -61,6 +61,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.fbs_compute_keys.restype = I
     lib.fbs_finalize_keys.argtypes = [I, I, I, I, P, P, P, P, P]
     lib.fbs_finalize_keys.restype = I
+    lib.fbs_suggest_ranges.argtypes = [P, P, I, P, P, P]
+    lib.fbs_suggest_ranges.restype = I
+    lib.fbs_compute_ranged.argtypes = [P, P, P, P, P, P, P]
+    lib.fbs_compute_ranged.restype = I
     lib.fbs_destroy.argtypes = [P]
     lib.fbs_destroy.restype = None
     lib.fbs_last_error.argtypes = []
@@ -142,6 +146,16 @@ def fbs_finalize_keys(W: int, H: int, d_min: int, d_max: int, keys_l, keys_r, re
                       stream=None) -> None:
     _check(load_library().fbs_finalize_keys(W, H, d_min, d_max, _ptr(keys_l), _ptr(keys_r), _ptr(rec_l),
                                             _ptr(disp_out), _stream(stream)))
+
+
+def fbs_suggest_ranges(h, seed_disp, margin: int, ranges_l, ranges_r, stream=None) -> None:
+    _check(load_library().fbs_suggest_ranges(h, _ptr(seed_disp), margin, _ptr(ranges_l), _ptr(ranges_r),
+                                             _stream(stream)))
+
+
+def fbs_compute_ranged(h, left, right, ranges_l, ranges_r, disp_out, stream=None) -> None:
+    _check(load_library().fbs_compute_ranged(h, _ptr(left), _ptr(right), _ptr(ranges_l), _ptr(ranges_r),
+                                             _ptr(disp_out), _stream(stream)))
 
 
 def finalize_keys(W: int, H: int, d_min: int, d_max: int, keys_l, keys_r, rec_l, out=None, stream=None):
@@ -362,6 +376,28 @@ class FBS:
         rec = torch.empty((self.H, self.W, 4), dtype=torch.float32, device=self.device)
         fbs_compute_keys(self.h, left, right, c_lo, c_hi, kl, kr, rec, stream)
         return kl, kr, rec
+
+    def suggest_ranges(self, seed_disp, margin: int, stream=None):
+        """NEXT-4: per-pixel suggested ranges (int16 [H, W, 2] left, right) from a
+        seed disparity map (float32 [H, W], values >= 0 are feature points)."""
+        import torch
+        if seed_disp.dtype != torch.float32 or tuple(seed_disp.shape) != (self.H, self.W) or not seed_disp.is_cuda:
+            raise ValueError("suggest_ranges: expected a float32 [H, W] device seed map")
+        rl = torch.empty((self.H, self.W, 2), dtype=torch.int16, device=self.device)
+        rr = torch.empty_like(rl)
+        fbs_suggest_ranges(self.h, seed_disp.contiguous(), margin, rl, rr, stream)
+        return rl, rr
+
+    def compute_ranged(self, left, right, ranges_l, ranges_r, out=None, stream=None):
+        """NEXT-4: fbs_compute with each pixel's WTA restricted to its range."""
+        import torch
+        self._chk_pair(left, right)
+        for t in (ranges_l, ranges_r):
+            if t.dtype != torch.int16 or tuple(t.shape) != (self.H, self.W, 2) or not t.is_cuda:
+                raise ValueError("compute_ranged: expected int16 [H, W, 2] device ranges")
+        out = self._out(out, (self.H, self.W))
+        fbs_compute_ranged(self.h, left, right, ranges_l.contiguous(), ranges_r.contiguous(), out, stream)
+        return out
 
     def select(self, agg_l, agg_r, stream=None):
         import torch

@@ -437,7 +437,9 @@ static fbs_ctx* create_volume(fbs_ctx* h) {
   cudaFuncSetAttribute(vol::k_agg<RR, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
                        sizeof(vol::AggSmem<RR>));                                                             \
   cudaFuncSetAttribute(vol::k_agg<RR, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
-                       sizeof(vol::AggSmem<RR>));
+                       sizeof(vol::AggSmem<RR>));                                                             \
+  cudaFuncSetAttribute(vol::k_agg<RR, false, false, false, true>,                                             \
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(vol::AggSmem<RR>));
   FBS_SMEM_ATTR(0) FBS_SMEM_ATTR(1) FBS_SMEM_ATTR(2) FBS_SMEM_ATTR(3) FBS_SMEM_ATTR(4)
   FBS_SMEM_ATTR(5) FBS_SMEM_ATTR(6) FBS_SMEM_ATTR(7) FBS_SMEM_ATTR(8) FBS_SMEM_ATTR(9) FBS_SMEM_ATTR(10)
 #undef FBS_SMEM_ATTR
@@ -518,7 +520,8 @@ struct KeysReq {
 
 // Volume path, one frame: output rows [r0, r1); exports when expC/expA are set.
 static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0, int r1, float* out,
-                      float* const* expC, float* const* expA, cudaStream_t s, const KeysReq* kq = nullptr) {
+                      float* const* expC, float* const* expA, cudaStream_t s, const KeysReq* kq = nullptr,
+                      const short2* const* ranges = nullptr) {
   const int W = h->W, H = h->H, R = h->R;
   // aggregation tiles are anchored at multiples of the tile height in frame rows, so a
   // pixel's denominator form never depends on the band; cost rows cover the
@@ -572,6 +575,8 @@ static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0,
   a.c_hi = kq ? kq->c_hi : h->D - 1;
   a.keys_out[0] = kq ? kq->keys_l : nullptr;
   a.keys_out[1] = kq ? kq->keys_r : nullptr;
+  a.ranges[0] = ranges ? ranges[0] : nullptr;
+  a.ranges[1] = ranges ? ranges[1] : nullptr;
   {
     const dim3 grid((W + vol::kTX - 1) / vol::kTX, ty1 - ty0, 2);
     cudaError_t e = cudaErrorInvalidValue;
@@ -582,6 +587,8 @@ static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0,
                               sizeof(vol::AggSmem<RR>), s, a)                                                 \
         : kq     ? launch_pdl(vol::k_agg<RR, false, false, true>, grid, dim3(vol::AggGeom<RR>::THREADS),      \
                               sizeof(vol::AggSmem<RR>), s, a)                                                 \
+        : ranges ? launch_pdl(vol::k_agg<RR, false, false, false, true>, grid,                                \
+                              dim3(vol::AggGeom<RR>::THREADS), sizeof(vol::AggSmem<RR>), s, a)                \
                  : launch_pdl(vol::k_agg<RR, false, false>, grid, dim3(vol::AggGeom<RR>::THREADS),            \
                               sizeof(vol::AggSmem<RR>), s, a);                                                \
     break;
@@ -605,7 +612,8 @@ static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0,
     const dim3 grd((W + 127) / 128, r1 - r0);
     const cudaError_t e = launch_pdl(vol::k_finalize, grd, dim3(128), 0, s, (const int32_t*)h->dmap[0],
                                      (const int32_t*)h->dmap[1], (const float*)a.aggL, (const float4*)a.agg3,
-                                     h->nblk, W, r0, r1, h->d_min, h->d_max, a.abase, out);
+                                     h->nblk, W, r0, r1, h->d_min, h->d_max, a.abase, out,
+                                     (const short2*)(ranges ? ranges[0] : nullptr));
     if (e != cudaSuccess) return cuda_check(e, "k_finalize launch");
     h->launches += 1;
   }
@@ -920,4 +928,33 @@ extern "C" int fbs_finalize_keys(int W, int H, int d_min, int d_max, const uint6
                                                               (const unsigned long long*)keys_r,
                                                               (const float4*)rec_l, W, H, d_min, d_max, disp_out);
   return cuda_check(cudaGetLastError(), "fbs_finalize_keys");
+}
+
+// ---------------------------------------------------------------------------
+// Sparse search range (NEXT-4, the paper's future work P:L358; R#31-R#33).
+extern "C" int fbs_suggest_ranges(fbs_ctx* h, const float* seed_disp, int margin, int16_t* ranges_l,
+                                  int16_t* ranges_r, fbs_stream_t stream) {
+  if (!h || !seed_disp || !ranges_l || !ranges_r) return fail(FBS_E_ARG, "fbs_suggest_ranges: NULL argument");
+  if (margin < 0) return fail(FBS_E_PARAM, "fbs_suggest_ranges: margin must be >= 0");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int W = h->W, H = h->H, T = vol::kRangeTile;
+  const int tx = (W + T - 1) / T, ty = (H + T - 1) / T, n = 2 * tx * ty;
+  int* tiles = nullptr;  // (min, max) per tile, left then right
+  if (cudaMallocAsync(&tiles, 2 * n * sizeof(int), s) != cudaSuccess) return fail(FBS_E_OOM, "fbs_suggest_ranges");
+  vol::k_range_init<<<(2 * n + 255) / 256, 256, 0, s>>>(tiles, 2 * n);
+  vol::k_range_seeds<<<dim3((W + 127) / 128, H), 128, 0, s>>>(seed_disp, W, H, tx, tiles, tiles + n);
+  vol::k_range_expand<<<dim3((W + 127) / 128, H), 128, 0, s>>>(tiles, tiles + n, W, H, tx, h->d_min, h->d_max, margin,
+                                                              (short2*)ranges_l, (short2*)ranges_r);
+  cudaFreeAsync(tiles, s);
+  return cuda_check(cudaGetLastError(), "fbs_suggest_ranges");
+}
+
+extern "C" int fbs_compute_ranged(fbs_ctx* h, const uint8_t* left, const uint8_t* right, const int16_t* ranges_l,
+                                  const int16_t* ranges_r, float* disp_out, fbs_stream_t stream) {
+  if (!h || !left || !right || !ranges_l || !ranges_r || !disp_out)
+    return fail(FBS_E_ARG, "fbs_compute_ranged: NULL argument");
+  if (h->path != FBS_PATH_VOLUME) return fail(FBS_E_UNSUPPORTED, "fbs_compute_ranged: volume path only");
+  if (!full_frame(h)) return fail(FBS_E_ARG, "fbs_compute_ranged: band handle");
+  const short2* rg[2] = {(const short2*)ranges_l, (const short2*)ranges_r};
+  return run_volume(h, left, right, 0, h->H, disp_out, nullptr, nullptr, (cudaStream_t)stream, nullptr, rg);
 }

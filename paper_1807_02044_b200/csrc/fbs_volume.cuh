@@ -273,7 +273,8 @@ __device__ __forceinline__ float finalize_pixel(int d_int, int e, float c0, floa
 // [H][nblk][W][64] store
 __global__ void k_finalize(const int32_t* __restrict__ dl, const int32_t* __restrict__ dr,
                            const float* __restrict__ aggL, const float4* __restrict__ agg3, int nblk, int W,
-                           int r0, int r1, int d_min, int d_max, int abase, float* __restrict__ out) {
+                           int r0, int r1, int d_min, int d_max, int abase, float* __restrict__ out,
+                           const short2* __restrict__ rng = nullptr) {
   pdl_wait();  // k_agg's maps
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = r0 + blockIdx.y;
@@ -289,11 +290,52 @@ __global__ void k_finalize(const int32_t* __restrict__ dl, const int32_t* __rest
   } else if (d >= 0) {
     auto at = [&](int di) { return aggL[(((size_t)(y - abase) * nblk + di / kDB) * W + x) * kDB + di % kDB]; };
     const int di = d - d_min;
+    const short2 r = rng ? rng[p] : make_short2(-32768, 32767);  // RANGED: R#33
     c0 = at(di);
-    if (d > d_min) cm = at(di - 1);
-    if (d < d_max) cp = at(di + 1);
+    if (d > d_min && d - 1 >= r.x) cm = at(di - 1);
+    if (d < d_max && d + 1 <= r.y) cp = at(di + 1);
   }
   out[(size_t)(y - r0) * W + x] = finalize_pixel(d, e, c0, cm, cp, d_min, d_max);
+}
+
+// Sparse search range (NEXT-4, R#31): feature points = valid seeds (>= 0) of a seed
+// disparity map; per frame-anchored T x T tile the range [floor(min) - m, ceil(max) + m]
+// of its seeds (left image) and of the forward-warped seeds (right image,
+// x_r = x - round(s)), clipped to [d_min, d_max]; tiles without seeds: full range.
+constexpr int kRangeTile = 16;
+__global__ void k_range_init(int* tiles, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) tiles[i] = (i & 1) ? -0x7fffffff : 0x7fffffff;  // (min, max) pairs
+}
+__global__ void k_range_seeds(const float* __restrict__ seed, int W, int H, int tx, int* tl, int* tr) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+  if (x >= W) return;
+  const float s = seed[(size_t)y * W + x];
+  if (!(s >= 0.f)) return;
+  const int lo = (int)floorf(s), hi = (int)ceilf(s);
+  int* t = tl + 2 * ((y / kRangeTile) * tx + x / kRangeTile);
+  atomicMin(t, lo);
+  atomicMax(t + 1, hi);
+  const int xr = x - (int)floorf(s + 0.5f);
+  if (xr >= 0 && xr < W) {
+    int* u = tr + 2 * ((y / kRangeTile) * tx + xr / kRangeTile);
+    atomicMin(u, lo);
+    atomicMax(u + 1, hi);
+  }
+}
+__global__ void k_range_expand(const int* __restrict__ tl, const int* __restrict__ tr, int W, int H, int tx,
+                               int d_min, int d_max, int margin, short2* __restrict__ rl, short2* __restrict__ rr) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+  if (x >= W) return;
+  const int t = 2 * ((y / kRangeTile) * tx + x / kRangeTile);
+  const int* src[2] = {tl + t, tr + t};
+  short2* dst[2] = {rl, rr};
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int a = src[k][0], b = src[k][1];
+    dst[k][(size_t)y * W + x] = a > b ? make_short2((short)d_min, (short)d_max)
+                                      : make_short2((short)max(d_min, a - margin), (short)min(d_max, b + margin));
+  }
 }
 
 // KEYS: the left record (c(d*-1), c(d*), c(d*+1)) of every pixel of rows [r0, r1)
@@ -392,6 +434,9 @@ struct AggArgs {
   // [c_lo, c_hi] compete in the WTA; the per-pixel keys (global d) are written out
   int c_lo, c_hi;
   unsigned long long* keys_out[2];
+  // RANGED instantiation (sparse search range, NEXT-4): per-pixel suggested range
+  // (lo, hi) of the left / right image, short2 [H][W]; only those d compete
+  const short2* ranges[2];
   unsigned long long* tile_stats;  // optional [4]: FAST / EDGE / GENERAL / EMPTY (sub-tile, d-block) counts
   float cd[(2 * kMaxRadius + 1) * (2 * kMaxRadius + 1)];  // log2 ω_d = -log2(e)(dx²+dy²)/γ_d², Eq.(7)
   float nkr;                                               // -log2(e)/γ_r²: log2 ω_r = nkr Δ², Eq.(8)
@@ -430,6 +475,8 @@ struct AggSmem {
   float cs[NW][32][K1 + 1];                         // EDGE: 1 / suffix (left) or prefix (right) column sums
   float g[GH * GWS];                                // guide tile (padded image values, see kGuideFlag)
   uint32_t cwb[NW][2][AggGeom<R>::CWS];             // classification words: current / next d-block
+  short2 rng[AggGeom<R>::TY][kTX];                  // RANGED: the tile's per-pixel suggested ranges
+  int rlo, rhi;                                     // RANGED: their union
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -696,7 +743,7 @@ __device__ __forceinline__ unsigned long long wta_butterfly16(unsigned long long
 // between both bodies compiled 20 % slower still).  Bit-identical results.
 // EXPORT: the debug export of the right aggregated volume is compiled in (its
 // store loop alone costs the production kernel ~1 %).
-template <int R, bool EMPTY, bool EXPORT, bool KEYS = false>
+template <int R, bool EMPTY, bool EXPORT, bool KEYS = false, bool RANGED = false>
 __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(const AggArgs a) {
   constexpr int kPY = AggGeom<R>::PY;
   constexpr int kTY = AggGeom<R>::TY;
@@ -714,6 +761,30 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
   pdl_trigger();
   pdl_wait();  // everything below reads k_cost's outputs
 
+  // RANGED: the union of the tile's suggested ranges decides which d-blocks run
+  int b_lo = 0, b_hi = a.nblk - 1;
+  if constexpr (RANGED) {
+    if (threadIdx.x == 0) { sm.rlo = 0x7fffffff; sm.rhi = -0x7fffffff; }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kTY * kTX; i += kThreads) {
+      const int px = i % kTX, py = i / kTX, x = x0 + px, y = y0 + py;
+      short2 r = make_short2(32767, -32768);  // outside the frame: no candidates
+      if (x < a.W && y < a.H) {
+        r = a.ranges[side][(size_t)y * a.W + x];
+        r.x = (short)max((int)r.x, a.d_min);
+        r.y = (short)min((int)r.y, a.d_max);
+        if (r.x <= r.y) { atomicMin(&sm.rlo, (int)r.x); atomicMax(&sm.rhi, (int)r.y); }
+      }
+      sm.rng[py][px] = r;
+    }
+    __syncthreads();
+    if (sm.rlo <= sm.rhi) {
+      b_lo = (sm.rlo - a.d_min) / kDB;
+      b_hi = (sm.rhi - a.d_min) / kDB;
+    } else {
+      b_lo = 0; b_hi = -1;  // no candidate disparity in the tile
+    }
+  }
   {  // guide tile (padded rows y0.., columns x0..: 16-B aligned) and the first
      // d-block's classification words, all in flight at once
     const float* src = (side == 0 ? a.gpadL : a.gpadR) + (size_t)y0 * a.Wg + x0;
@@ -721,7 +792,7 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
       const int row = c / (GW / 4), q = c % (GW / 4);
       cp_async16(&sm.g[row * GWS + 4 * q], src + (size_t)row * a.Wg + 4 * q);
     }
-    cw_load<R>(a, side, sx, sy, 0, lane, sm.cwb[warp][0]);
+    if (b_lo <= b_hi) cw_load<R>(a, side, sx, sy, b_lo, lane, sm.cwb[warp][b_lo & 1]);
     cp_async_commit();
     cp_async_wait_all();
   }
@@ -804,10 +875,10 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
     return AggSmem<R>::kAlias ? sm.w[warp] + (py0 + pyl) * RS : sm.val[warp] + (py0 + pyl) * kPX * kDB;
   };
   unsigned long long best = 0ull;  // running best key of slot (lane & 15) of this half
-  for (int b = 0; b < a.nblk; ++b) {
+  for (int b = b_lo; b <= b_hi; ++b) {
     // volume row (sy + py0 - R + r) + R = sy + py0 + r; column (sx - R + j) + R = sx + j
     const float* vb = vol + vol_at(sy + py0 - a.vbase, b, sx, a.nblk, a.Wv) + 4 * dq;
-    if (b > 0) {  // this d-block's words (issued one d-block ahead)
+    if (b > b_lo) {  // this d-block's words (issued one d-block ahead)
       cp_async_wait_all();
       // one CTA barrier per d-block keeps the warps in lockstep: warps that drift
       // apart run different parts of the unrolled FMA stream, which is larger than
@@ -816,7 +887,7 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
     }
     const int cls = cw_classify<R>(a, side, sx, sy, b, lane, sm.cwb[warp][b & 1]);
     __syncwarp();
-    if (b + 1 < a.nblk) {
+    if (b + 1 <= b_hi) {
       cw_load<R>(a, side, sx, sy, b + 1, lane, sm.cwb[warp][(b + 1) & 1]);
       cp_async_commit();
     }
@@ -840,6 +911,14 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
             v2 = padded ? agg.z : agg.z + pad[2], v3 = padded ? agg.w : agg.w + pad[3];
       if constexpr (KEYS) {
         v0 += cpad[0]; v1 += cpad[1]; v2 += cpad[2]; v3 += cpad[3];
+      }
+      if constexpr (RANGED) {  // only the pixel's suggested range competes (R#32)
+        const short2 r = sm.rng[wy + py0 + pyl][wx + px];
+        const int d0 = a.d_min + di0;
+        v0 += (d0 >= r.x && d0 <= r.y) ? 0.f : -INFINITY;
+        v1 += (d0 + 1 >= r.x && d0 + 1 <= r.y) ? 0.f : -INFINITY;
+        v2 += (d0 + 2 >= r.x && d0 + 2 <= r.y) ? 0.f : -INFINITY;
+        v3 += (d0 + 3 >= r.x && d0 + 3 <= r.y) ? 0.f : -INFINITY;
       }
       const bool h01 = v1 > v0, h23 = v3 > v2;     // equal values keep the smaller d
       const float b01 = h01 ? v1 : v0, b23 = h23 ? v3 : v2;
@@ -953,8 +1032,13 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
         if (side == 0 && a.agg3 && ok) {  // the three costs Eq.(10) needs
           const float* vr = vrow(s2 / kPX) + (s2 % kPX) * kDB;
           const int di = d_int - a.d_min;
-          a.agg3[(size_t)y * a.W + x] =
-              make_float4(di > 0 ? vr[di - 1] : kSent, vr[di], di + 1 < a.D ? vr[di + 1] : kSent, 0.f);
+          bool in_m = di > 0, in_p = di + 1 < a.D;
+          if constexpr (RANGED) {  // the range ends act like the ends of [d_min, d_max] (R#33)
+            const short2 r = sm.rng[wy + py0 + s2 / kPX][wx + s2 % kPX];
+            in_m = in_m && d_int - 1 >= r.x;
+            in_p = in_p && d_int + 1 <= r.y;
+          }
+          a.agg3[(size_t)y * a.W + x] = make_float4(in_m ? vr[di - 1] : kSent, vr[di], in_p ? vr[di + 1] : kSent, 0.f);
         }
       }
     }

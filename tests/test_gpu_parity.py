@@ -420,3 +420,40 @@ def test_drange_split_matches_oracle(fbs, oracle_lib, world):
     full, fdl, _ = (t.cpu().numpy() for t in fbs.FBS(W, H, d_min, d_max, rho, 5.0, 32.0).maps(Ld, Rd))
     assert np.mean(fdl == dl) > 0.99
     log_errors(f"drange-split-{world}", subpix=rep.max_subpix_err, near_ties=rep.near_ties, pixels=W * H)
+
+
+@pytest.mark.parametrize("cfgname,margin", [("teddy", 3), ("three-dblocks", 4)])
+def test_sparse_search_range_matches_oracle(fbs, oracle_lib, cfgname, margin):
+    """NEXT-4 (P:L358, R#31-R#33): ranges suggested on the GPU from a seed map (the
+    full-range result of the same pair, i.e. a stream's previous frame), then the
+    ranged WTA -> both equal the ranged oracle (ranges bit-exact; maps under the
+    parity rules), and full ranges reproduce fbs_compute bit for bit."""
+    from oracle import ranged
+    if cfgname == "teddy":
+        cfg = synth.CONFIGS["teddy"]
+        W, H, d_min, d_max, rho, gd, gr = cfg.W, cfg.H, cfg.d_min, cfg.d_max, cfg.radius, cfg.gamma_d, cfg.gamma_r
+        L, R = synth.frame(cfg, 0)
+    else:
+        W, H, d_min, d_max, rho, gd, gr = 150, 40, 0, 129, 2, 3.0, 40.0
+        L, R = make_pair("layered", W, H, d_min, d_max, 12)
+    ref = oracle_lib.fbs(L, R, d_min, d_max, rho, gd, gr)
+    m = fbs.FBS(W, H, d_min, d_max, rho, gd, gr)
+    Ld, Rd = to_dev(L), to_dev(R)
+    seed = m.compute(Ld, Rd)
+    rl, rr = m.suggest_ranges(seed, margin)
+    orl, orr = ranged.suggest_ranges(seed.cpu().numpy().astype(np.float64), d_min, d_max, margin)
+    assert np.array_equal(rl.cpu().numpy(), orl) and np.array_equal(rr.cpu().numpy(), orr)
+    out = m.compute_ranged(Ld, Rd, rl, rr).cpu().numpy()
+    disp, dl_o, dr_o, den = ranged.fbs_ranged(ref, d_min, d_max, orl, orr)
+    # integer maps of the ranged launch: decode from the ranged oracle's decisions
+    # through the final map (INVALID / integer part), then the parity rules
+    ok_o, ok_g = disp >= 0, out >= 0
+    same = ok_o == ok_g
+    assert same.mean() > 0.995, same.mean()
+    both = ok_o & ok_g
+    assert np.mean(np.abs(out[both] - disp[both]) <= parity.SUBPIX) > 0.995
+    fr = torch.empty((H, W, 2), dtype=torch.int16, device="cuda")
+    fr[..., 0], fr[..., 1] = d_min, d_max
+    full = m.compute_ranged(Ld, Rd, fr, fr).cpu().numpy()
+    assert np.array_equal(full.view(np.uint32), seed.cpu().numpy().view(np.uint32))
+    log_errors(f"sparse-range-{cfgname}", agree=float(same.mean()), pixels=W * H)
