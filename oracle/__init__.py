@@ -16,6 +16,8 @@ Parity status per function (DESIGN.md §4 lists the pins):
                                   natural-like scenes beyond those: parity
                                   unpinned (no reference values exist).
   fbs_pixels                      pinned against fbs (bit-identical).
+  ranged.* (sparse search range)  pinned (tests/test_oracle_ranged.py): reduces to
+                                  fbs with full ranges; closed forms; known shift.
 """
 from __future__ import annotations
 
