@@ -14,8 +14,9 @@
 //                           WTA butterfly, per-pixel record.
 // The ring holds NS = 3 CY + 2ρ rows, so while the two consumer groups work on
 // chunks c and c+1 the producers already write chunk c+2.  Hand-over: mbarriers
-// full[c mod 4] (producers -> group, one arrival) and empty[c mod 4] (group ->
-// producers, one arrival per consumer warp); TMA completion on tbar[phase mod 2].
+// full[c mod 4] (producers -> group) and empty_ring / empty_w[c mod 4] (group ->
+// producers), each arrived on by every thread of the signalling side; TMA
+// completion on tbar[phase mod 3].
 //
 // Ordering rules (c = chunk counter of the CTA, the same in every warp):
 //   * chunk c's new cost rows overwrite the rows of chunk c-3's window, so the
@@ -208,9 +209,12 @@ __global__ void __launch_bounds__(SGeo<R>::THREADS, 1) k_fbs_ws(const __grid_con
     mbar_init(&sm.tbar[2], 1);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      mbar_init(&sm.full[i], 1);
-      mbar_init(&sm.empty_ring[i], 4);
-      mbar_init(&sm.empty_w[i], 4);
+      // every thread that wrote (or read) the hand-over data arrives itself, so the
+      // release -> acquire edge is direct for each of them (no reliance on a
+      // named barrier or __syncwarp in between; racecheck-clean)
+      mbar_init(&sm.full[i], G::NPW * 32);
+      mbar_init(&sm.empty_ring[i], 4 * 32);
+      mbar_init(&sm.empty_w[i], 4 * 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 #pragma unroll
@@ -334,7 +338,7 @@ __global__ void __launch_bounds__(SGeo<R>::THREADS, 1) k_fbs_ws(const __grid_con
       named_sync(1, G::NPW * 32);  // the phase's rows / weights are written; its staging buffer is free
       if (tr) tr[3] = clock64() | ((unsigned long long)chunk << 63);
       if (chunk) {
-        if (leader) mbar_arrive(&sm.full[c & 3]);
+        mbar_arrive(&sm.full[c & 3]);
         ++c;
         if (++wb == 3) wb = 0;
       }
@@ -421,7 +425,7 @@ __global__ void __launch_bounds__(SGeo<R>::THREADS, 1) k_fbs_ws(const __grid_con
         for (int px = 0; px < kPX; ++px) num[py][px][0] = num[py][px][1] = make_float2(0.f, 0.f);
       if (!(FBS_ABL & 2)) ring_stream<G, HPY>(col, base, wsm, num);
       __syncwarp();  // every lane is done with the ring and the weights
-      if (lane == 0) mbar_arrive(&sm.empty_ring[cc & 3]);
+      mbar_arrive(&sm.empty_ring[cc & 3]);
 #pragma unroll
       for (int pyl = 0; pyl < HPY; ++pyl)
 #pragma unroll
@@ -449,7 +453,7 @@ __global__ void __launch_bounds__(SGeo<R>::THREADS, 1) k_fbs_ws(const __grid_con
                                     __fmaf_rn(n1.x, ri[2], off[2]), __fmaf_rn(n1.y, ri[3], off[3])), true);
         }
     } else if (cls == kEmpty) {
-      if (lane == 0) mbar_arrive(&sm.empty_ring[cc & 3]);
+      mbar_arrive(&sm.empty_ring[cc & 3]);
 #pragma unroll
       for (int pyl = 0; pyl < HPY; ++pyl)
 #pragma unroll
@@ -465,7 +469,7 @@ __global__ void __launch_bounds__(SGeo<R>::THREADS, 1) k_fbs_ws(const __grid_con
         ring_num_den_row<G>(col, bb, wsm + pyl * RS, num[pyl], den[pyl]);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.empty_ring[cc & 3]);
+      mbar_arrive(&sm.empty_ring[cc & 3]);
 #pragma unroll
       for (int pyl = 0; pyl < HPY; ++pyl)
 #pragma unroll
@@ -513,7 +517,7 @@ __global__ void __launch_bounds__(SGeo<R>::THREADS, 1) k_fbs_ws(const __grid_con
       }
     }
     __syncwarp();  // vrow (the weight buffer) is read before it is handed back
-    if (lane == 0) mbar_arrive(&sm.empty_w[cc & 3]);
+    mbar_arrive(&sm.empty_w[cc & 3]);
     if (tr) tr[3] = clock64();
   }
 }
