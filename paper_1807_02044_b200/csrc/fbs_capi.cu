@@ -373,6 +373,11 @@ static fbs_ctx* create_impl(int W, int H, int d_min, int d_max, int radius, floa
   return h;
 }
 
+// Production k_agg instantiation has the EMPTY denominator form (units whose costs are
+// all undefined skip the stream): KITTI 1,295 -> 1,586 frames/s, Teddy -0.6 %,
+// MB2014 -1.9 % (interleaved A/B).
+static constexpr bool kVolEmpty = true;
+
 // Volume path scratch (one frame): FBS_PATH_VOLUME.
 static fbs_ctx* create_volume(fbs_ctx* h) {
   const int W = h->W, H = h->H, R = h->R;
@@ -432,7 +437,7 @@ static fbs_ctx* create_volume(fbs_ctx* h) {
   // fixed per instantiation (k_cost: the largest supported block count), so a later
   // handle never lowers another handle's cap
 #define FBS_SMEM_ATTR(RR)                                                                                     \
-  cudaFuncSetAttribute(vol::k_agg<RR, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,             \
+  cudaFuncSetAttribute(vol::k_agg<RR, kVolEmpty, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
                        sizeof(vol::AggSmem<RR>));                                                             \
   cudaFuncSetAttribute(vol::k_agg<RR, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
                        sizeof(vol::AggSmem<RR>));                                                             \
@@ -589,7 +594,7 @@ static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0,
                               sizeof(vol::AggSmem<RR>), s, a)                                                 \
         : ranges ? launch_pdl(vol::k_agg<RR, false, false, false, true>, grid,                                \
                               dim3(vol::AggGeom<RR>::THREADS), sizeof(vol::AggSmem<RR>), s, a)                \
-                 : launch_pdl(vol::k_agg<RR, false, false>, grid, dim3(vol::AggGeom<RR>::THREADS),            \
+                 : launch_pdl(vol::k_agg<RR, kVolEmpty, false>, grid, dim3(vol::AggGeom<RR>::THREADS),        \
                               sizeof(vol::AggSmem<RR>), s, a);                                                \
     break;
       FBS_CASE(0) FBS_CASE(1) FBS_CASE(2) FBS_CASE(3) FBS_CASE(4) FBS_CASE(5) FBS_CASE(6)
