@@ -45,6 +45,9 @@ CASES = [
     ("gamma-r28-bound", 96, 64, 0, 31, 4, "half", 21, 5.0, 28.0),
     ("gamma-r30-rho6", 96, 64, 0, 31, 6, "half", 22, 3.0, 30.0),
     ("gamma-d-small", 96, 64, 0, 31, 3, "half", 23, 0.7, 40.0),
+    # SPEC's box limit (γ_d, γ_r -> ∞: every weight 1, Eq.(6) is the plain average of
+    # the defined costs); runs since the γ_r cap is gone (R#13)
+    ("box-limit", 64, 48, 0, 15, 3, "half", 24, 1e9, 1e9),
 ]
 
 
