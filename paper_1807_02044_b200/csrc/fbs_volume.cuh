@@ -736,13 +736,13 @@ __device__ __forceinline__ unsigned long long wta_butterfly16(unsigned long long
 }
 
 // grid: (ceil(W/kTX), tile rows, 2 sides); block AggGeom<R>::THREADS (warps of 4 x PY sub-tiles).
-// EMPTY: whether GENERAL units test for the EMPTY special case (fbs_create reads
-// FBS_EMPTY_FORM).  A separate instantiation because the test perturbs the
-// code generated for the FAST stream: measured 3.5 % slower at Teddy, 19 %
-// faster on KITTI-shaped streams with textureless frames (an in-kernel switch
-// between both bodies compiled 20 % slower still).  Bit-identical results.
+// EMPTY: whether GENERAL units test for the EMPTY special case (the production
+// instantiation does: KITTI +22.5 %, Teddy -0.6 %).  Bit-identical
+// results either way.
 // EXPORT: the debug export of the right aggregated volume is compiled in (its
 // store loop alone costs the production kernel ~1 %).
+// KEYS: disparity-range split (fbs_compute_keys); RANGED: sparse search range
+// (fbs_compute_ranged).
 template <int R, bool EMPTY, bool EXPORT, bool KEYS = false, bool RANGED = false>
 __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(const AggArgs a) {
   constexpr int kPY = AggGeom<R>::PY;

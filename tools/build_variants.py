@@ -1,5 +1,5 @@
 """Build experimental libfbs variants (paper_1807_02044_b200/libfbs_exp_<name>.so) from
--D flag sets, for A/B runs with FBS_LIB (tools/gpu_ab.sh).  Usage:
+-D flag sets, for A/B runs with FBS_LIB (tools/gpu.sh ab).  Usage:
   python tools/build_variants.py name1='-DFOO=1 -DBAR=2' name2='...'"""
 import os
 import subprocess
