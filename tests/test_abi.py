@@ -89,7 +89,26 @@ def test_null_handle_calls_fail_cleanly(lib):
     assert lib.fbs_compute(None, None, None, None, None) == -1
     assert lib.fbs_compute_rows(None, None, None, 0, 1, None, None) == -1
     assert lib.fbs_stats(None, None) == -1
+    assert lib.fbs_compute_keys(None, None, None, 0, 1, None, None, None, None) == -1
+    assert lib.fbs_finalize_keys(10, 10, 0, 5, None, None, None, None, None) == -1
+    assert lib.fbs_suggest_ranges(None, None, 2, None, None, None) == -1
+    assert lib.fbs_compute_ranged(None, None, None, None, None, None, None) == -1
     lib.fbs_destroy(None)
+
+
+@pytest.mark.parametrize("args", [
+    (10, 10, 0, 5, 1, 5.0, 40.0, 2),          # unknown path
+    (10, 10, 0, 5, 7, 5.0, 40.0, 1),          # radius > 6 on the fused path
+])
+def test_create_ex_rejects(lib, args):
+    assert not lib.fbs_create_ex(*args)
+    assert lib.fbs_last_error().decode().startswith("fbs_create")
+
+
+@pytest.mark.parametrize("rows", [(-1, 5), (5, 5), (3, 11)])
+def test_create_band_rejects_bad_rows(lib, rows):
+    assert not lib.fbs_create_band(10, 10, 0, 5, 1, 5.0, 40.0, 0, *rows)
+    assert lib.fbs_last_error().decode().startswith("fbs_create_band")
 
 
 def test_binding_fails_loudly_without_library(tmp_path):
