@@ -20,4 +20,9 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_co
   python bench.py --path volume --steps 3 --warmup 3 --no-extras --no-graph > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_fbs_ws -s 2 -c 1 -o $o/prof_fbsws_teddy -f \
   python bench.py --path fused --steps 3 --warmup 3 --no-extras --no-graph > /dev/null 2>&1
-ls -la $o
+# summarise the captures here (the .ncu-rep files are too large to bring back)
+mkdir -p gpurun_out/r02_summary
+cp profiles/ncu_summary.json gpurun_out/r02_summary/ 2>/dev/null
+python tools/make_profiles.py r02 $o --out gpurun_out/r02_summary > gpurun_out/r02_summary/make_profiles.log 2>&1
+mkdir -p /tmp/ncu_reps && mv $o/*.ncu-rep /tmp/ncu_reps/ 2>/dev/null
+ls -la $o gpurun_out/r02_summary

@@ -8,7 +8,9 @@ summaries under profiles/ (round-tagged):
   profiles/ncu_summary.json           per-launch DRAM bytes of the aggregation kernel
                                       (bench.py's roofline "traffic")
 
-usage: python tools/make_profiles.py <tag> [gpurun_out]
+usage: python tools/make_profiles.py <tag> [gpurun_out/<tag>] [--out DIR]
+(--out: write the summaries elsewhere, e.g. on the GPU box into gpurun_out/, whose
+.ncu-rep files are too large to bring back)
 """
 import collections
 import csv
@@ -43,9 +45,14 @@ CAPTURES = (("agg", "prof_agg_teddy", "volume"), ("cost", "prof_cost_teddy", "vo
 
 
 def main():
-    tag = sys.argv[1]
-    src = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out", tag)
+    args = [a for a in sys.argv[1:]]
     out = os.path.join(ROOT, "profiles")
+    if "--out" in args:
+        i = args.index("--out")
+        out = args[i + 1]
+        del args[i:i + 2]
+    tag = args[0]
+    src = args[1] if len(args) > 1 else os.path.join(ROOT, "gpurun_out", tag)
     os.makedirs(out, exist_ok=True)
     sp = os.path.join(out, "ncu_summary.json")
     summary = json.load(open(sp)) if os.path.exists(sp) else {}
