@@ -147,6 +147,19 @@ int fbs_compute_rows(fbs_ctx* h, const uint8_t* left, const uint8_t* right, int 
                      int row_end, float* disp_band, fbs_stream_t stream);
 
 /*
+ * fbs_compute_rows_scatter — fbs_compute_rows whose final-map kernel stores each
+ * pixel of rows [row_begin, row_end) into every one of `nouts` (1..8) full-frame
+ * buffers (device float [H][W], frame coordinates) instead of a band buffer: the
+ * WTA epilogue's band scatter of the row-band partitioner (NEXT-3).  With the
+ * peers' symmetric-memory buffers (mapped into this GPU's address space) the
+ * stores go over NVLink and replace the all-gather; `outs` is a host array of
+ * device pointers.  Rows outside the band are not touched.  Asynchronous; the
+ * caller synchronises the ranks (e.g. a symmetric-memory barrier) before reading.
+ */
+int fbs_compute_rows_scatter(fbs_ctx* h, const uint8_t* left, const uint8_t* right, int row_begin,
+                             int row_end, float* const* outs, int nouts, fbs_stream_t stream);
+
+/*
  * fbs_compute_batch — n independent pairs, frame i at left + i*H*W,
  * right + i*H*W, output at disp_out + i*H*W (all device).  Equivalent to n
  * fbs_compute calls in order on `stream`.  n >= 1.

@@ -27,7 +27,7 @@ FBS_PATH_VOLUME, FBS_PATH_FUSED = 0, 1
 PATHS = {"volume": FBS_PATH_VOLUME, "fused": FBS_PATH_FUSED}
 
 # every symbol include/fbs.h declares
-EXPORTS = ("fbs_create", "fbs_create_ex", "fbs_create_band", "fbs_compute_keys", "fbs_finalize_keys", "fbs_suggest_ranges", "fbs_compute_ranged", "fbs_destroy", "fbs_last_error", "fbs_compute", "fbs_compute_rows",
+EXPORTS = ("fbs_create", "fbs_create_ex", "fbs_create_band", "fbs_compute_rows_scatter", "fbs_compute_keys", "fbs_finalize_keys", "fbs_suggest_ranges", "fbs_compute_ranged", "fbs_destroy", "fbs_last_error", "fbs_compute", "fbs_compute_rows",
            "fbs_compute_batch", "fbs_compute_host", "fbs_compute_host_batch", "fbs_debug_volumes", "fbs_debug_select",
            "fbs_debug_maps", "fbs_stats", "fbs_profile_enable", "fbs_profile_read", "fbs_tile_stats")
 FBS_NSTAGES = 3
@@ -71,6 +71,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.fbs_last_error.restype = ctypes.c_char_p
     lib.fbs_compute.argtypes = [P, P, P, P, P]
     lib.fbs_compute_rows.argtypes = [P, P, P, I, I, P, P]
+    lib.fbs_compute_rows_scatter.argtypes = [P, P, P, I, I, P, I, P]
+    lib.fbs_compute_rows_scatter.restype = I
     lib.fbs_compute_batch.argtypes = [P, P, P, I, P, P]
     lib.fbs_compute_host.argtypes = [P, P, P, P, P]
     lib.fbs_compute_host_batch.argtypes = [P, P, P, I, P, P]
@@ -182,6 +184,13 @@ def fbs_compute(h, left, right, disp_out, stream=None) -> None:
 def fbs_compute_rows(h, left, right, row_begin: int, row_end: int, disp_band, stream=None) -> None:
     _check(load_library().fbs_compute_rows(h, _ptr(left), _ptr(right), row_begin, row_end,
                                            _ptr(disp_band), _stream(stream)))
+
+
+def fbs_compute_rows_scatter(h, left, right, row_begin: int, row_end: int, out_ptrs, stream=None) -> None:
+    """out_ptrs: device addresses (ints) of full-frame float32 [H][W] buffers."""
+    arr = (ctypes.c_void_p * len(out_ptrs))(*[ctypes.c_void_p(int(p)) for p in out_ptrs])
+    _check(load_library().fbs_compute_rows_scatter(h, _ptr(left), _ptr(right), row_begin, row_end, arr,
+                                                   len(out_ptrs), _stream(stream)))
 
 
 def fbs_compute_batch(h, left, right, n: int, disp_out, stream=None) -> None:
@@ -319,6 +328,16 @@ class FBS:
         out = self._out(out, (r1 - r0, self.W))
         fbs_compute_rows(self.h, left, right, r0, r1, out, stream)
         return out
+
+    def compute_rows_scatter(self, left, right, r0: int, r1: int, out_ptrs, stream=None):
+        """Rows [r0, r1) stored into every full-frame buffer of out_ptrs (device
+        addresses of float32 [H, W] buffers, e.g. symmetric-memory peers)."""
+        self._chk_pair(left, right)
+        if not self.rows[0] <= r0 < r1 <= self.rows[1]:
+            raise ValueError(f"compute_rows_scatter: need {self.rows[0]} <= r0 < r1 <= {self.rows[1]}")
+        if not 1 <= len(out_ptrs) <= 8:
+            raise ValueError("compute_rows_scatter: 1..8 destination buffers")
+        fbs_compute_rows_scatter(self.h, left, right, r0, r1, out_ptrs, stream)
 
     def compute_batch(self, left, right, out=None, stream=None):
         n = left.shape[0]

@@ -63,6 +63,7 @@ struct fbs_ctx {
   unsigned long long* tile_stats;  // device [4] FAST/EDGE/GENERAL/EMPTY, counting while profiling
   unsigned long long* trace;       // FBS_TRACE builds: kernel timeline of CTA 0
   int launches;
+  OutSet scat;  // fbs_compute_rows_scatter: destinations of the current call (n = 0 otherwise)
   cudaEvent_t* prof_ev;  // live profiling (fbs_profile_enable): kEv events per call
   int prof_cap, prof_n;
 };
@@ -615,10 +616,11 @@ static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0,
   }
   {
     const dim3 grd((W + 127) / 128, r1 - r0);
-    const cudaError_t e = launch_pdl(vol::k_finalize, grd, dim3(128), 0, s, (const int32_t*)h->dmap[0],
+    const cudaError_t e = launch_pdl(h->scat.n ? vol::k_finalize<true> : vol::k_finalize<false>, grd, dim3(128), 0,
+                                     s, (const int32_t*)h->dmap[0],
                                      (const int32_t*)h->dmap[1], (const float*)a.aggL, (const float4*)a.agg3,
                                      h->nblk, W, r0, r1, h->d_min, h->d_max, a.abase, out,
-                                     (const short2*)(ranges ? ranges[0] : nullptr));
+                                     (const short2*)(ranges ? ranges[0] : nullptr), h->scat);
     if (e != cudaSuccess) return cuda_check(e, "k_finalize launch");
     h->launches += 1;
   }
@@ -683,8 +685,10 @@ static int run(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int nf, int r0
     h->launches += 1;
   }
   if (ev) cudaEventRecord(ev[2], s);
-  e = launch_pdl(k_final, dim3((W + 127) / 128, r1 - r0, nf), dim3(128), 0, s, (const int32_t*)h->dmap[0],
-                 (const int32_t*)h->dmap[1], (const float4*)h->agg3, W, H, r0, r1, h->d_min, h->d_max, out);
+  e = launch_pdl(h->scat.n ? k_final<true> : k_final<false>, dim3((W + 127) / 128, r1 - r0, nf), dim3(128), 0, s,
+                 (const int32_t*)h->dmap[0],
+                 (const int32_t*)h->dmap[1], (const float4*)h->agg3, W, H, r0, r1, h->d_min, h->d_max, out,
+                 h->scat);
   if (e != cudaSuccess) return cuda_check(e, "k_final launch");
   h->launches += 1;
   if (ev) cudaEventRecord(ev[3], s);
@@ -707,6 +711,24 @@ extern "C" int fbs_compute_rows(fbs_ctx* h, const uint8_t* left, const uint8_t* 
     return fail(FBS_E_ARG, "fbs_compute_rows: need rb0 <= row_begin < row_end <= rb1 (the handle's rows; [0, H) "
                            "unless created by fbs_create_band)");
   return run(h, left, right, 1, row_begin, row_end, disp_band, nullptr, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" int fbs_compute_rows_scatter(fbs_ctx* h, const uint8_t* left, const uint8_t* right, int row_begin,
+                                        int row_end, float* const* outs, int nouts, fbs_stream_t stream) {
+  if (!h || !left || !right || !outs) return fail(FBS_E_ARG, "fbs_compute_rows_scatter: NULL argument");
+  if (nouts < 1 || nouts > kMaxScatter) return fail(FBS_E_ARG, "fbs_compute_rows_scatter: need 1 <= nouts <= 8");
+  if (row_begin < h->rb0 || row_end > h->rb1 || row_begin >= row_end)
+    return fail(FBS_E_ARG, "fbs_compute_rows_scatter: rows outside the handle's band");
+  OutSet os{};
+  for (int k = 0; k < nouts; ++k) {
+    if (!outs[k]) return fail(FBS_E_ARG, "fbs_compute_rows_scatter: NULL destination");
+    os.p[k] = outs[k];
+  }
+  os.n = nouts;
+  h->scat = os;
+  const int rc = run(h, left, right, 1, row_begin, row_end, outs[0], nullptr, nullptr, (cudaStream_t)stream);
+  h->scat = OutSet{};
+  return rc;
 }
 
 extern "C" int fbs_compute_batch(fbs_ctx* h, const uint8_t* left, const uint8_t* right, int n,
@@ -827,8 +849,8 @@ extern "C" int fbs_debug_select(fbs_ctx* h, const float* agg_l, const float* agg
   k_select_wta<<<nb, 256, 0, s>>>(agg_r, h->W, h->H, h->D, h->d_min, h->dmap[1], nullptr);
   k_select_wta<<<nb, 256, 0, s>>>(agg_l, h->W, h->H, h->D, h->d_min, h->dmap[0], h->agg3);
   if (disp_out)
-    k_final<<<dim3((h->W + 127) / 128, h->H, 1), 128, 0, s>>>(h->dmap[0], h->dmap[1], h->agg3, h->W, h->H, 0, h->H,
-                                                              h->d_min, h->d_max, disp_out);
+    k_final<false><<<dim3((h->W + 127) / 128, h->H, 1), 128, 0, s>>>(h->dmap[0], h->dmap[1], h->agg3, h->W, h->H, 0, h->H,
+                                                              h->d_min, h->d_max, disp_out, OutSet{});
   if (disp_l) cudaMemcpyAsync(disp_l, h->dmap[0], npix * 4, cudaMemcpyDeviceToDevice, s);
   if (disp_r) cudaMemcpyAsync(disp_r, h->dmap[1], npix * 4, cudaMemcpyDeviceToDevice, s);
   return cuda_check(cudaGetLastError(), "fbs_debug_select");

@@ -829,9 +829,10 @@ __global__ void __launch_bounds__(256, 1) k_fbs(const __grid_constant__ WalkArgs
 
 // LRC (Eq.(9)) + subpixel (Eq.(10)) of rows [r0, r1) of frame blockIdx.z, from
 // the walker's maps and per-pixel record (c(d*-1), c(d*), c(d*+1)).
+template <bool SCATTER>
 __global__ void k_final(const int32_t* __restrict__ dl, const int32_t* __restrict__ dr,
                         const float4* __restrict__ agg3, int W, int H, int r0, int r1, int d_min, int d_max,
-                        float* __restrict__ out) {
+                        float* __restrict__ out, const OutSet os) {
   pdl_wait();  // the walker's maps
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = r0 + blockIdx.y;
@@ -845,7 +846,12 @@ __global__ void k_final(const int32_t* __restrict__ dl, const int32_t* __restric
     const float4 v = agg3[p];
     cm = v.x; c0 = v.y; cp = v.z;
   }
-  out[((size_t)blockIdx.z * (r1 - r0) + (y - r0)) * W + x] = finalize_pixel(d, e, c0, cm, cp, d_min, d_max);
+  const float v = finalize_pixel(d, e, c0, cm, cp, d_min, d_max);
+  if constexpr (!SCATTER) {
+    out[((size_t)blockIdx.z * (r1 - r0) + (y - r0)) * W + x] = v;
+  } else {
+    for (int k = 0; k < os.n; ++k) os.p[k][(size_t)y * W + x] = v;  // band scatter (one frame)
+  }
 }
 
 }  // namespace fbs

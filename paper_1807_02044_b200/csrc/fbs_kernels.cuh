@@ -65,6 +65,16 @@ __global__ void k_fill(float* p, size_t n, float v) {
     p[i] = v;
 }
 
+// Band scatter (fbs_compute_rows_scatter): the final map of the band's rows is
+// stored into every buffer of the set — full [H][W] frames, e.g. the peers'
+// symmetric-memory buffers mapped into this GPU (NVLink P2P stores) — instead
+// of the band-relative output; n = 0: the usual output.
+constexpr int kMaxScatter = 8;
+struct OutSet {
+  float* p[kMaxScatter];
+  int n;
+};
+
 // ---------------------------------------------------------------------------
 // Stage 4: Eq.(9) LRC (tolerance 1, R#17) then Eq.(10) subpixel on aggregated
 // costs (R#19, R#21).  d_int: left WTA disparity or -1; e: d_R(u - d_int, v) or -1.

@@ -271,10 +271,11 @@ __device__ __forceinline__ float finalize_pixel(int d_int, int e, float c0, floa
 
 // rows [r0, r1): out[(y - r0)*W + x]; aggregated costs from the left pass's
 // [H][nblk][W][64] store
+template <bool SCATTER>
 __global__ void k_finalize(const int32_t* __restrict__ dl, const int32_t* __restrict__ dr,
                            const float* __restrict__ aggL, const float4* __restrict__ agg3, int nblk, int W,
                            int r0, int r1, int d_min, int d_max, int abase, float* __restrict__ out,
-                           const short2* __restrict__ rng = nullptr) {
+                           const short2* __restrict__ rng, const OutSet os) {
   pdl_wait();  // k_agg's maps
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = r0 + blockIdx.y;
@@ -295,7 +296,12 @@ __global__ void k_finalize(const int32_t* __restrict__ dl, const int32_t* __rest
     if (d > d_min && d - 1 >= r.x) cm = at(di - 1);
     if (d < d_max && d + 1 <= r.y) cp = at(di + 1);
   }
-  out[(size_t)(y - r0) * W + x] = finalize_pixel(d, e, c0, cm, cp, d_min, d_max);
+  const float v = finalize_pixel(d, e, c0, cm, cp, d_min, d_max);
+  if constexpr (!SCATTER) {
+    out[(size_t)(y - r0) * W + x] = v;
+  } else {
+    for (int k = 0; k < os.n; ++k) os.p[k][p] = v;  // band scatter: frame coordinates
+  }
 }
 
 // Sparse search range (NEXT-4, R#31): feature points = valid seeds (>= 0) of a seed

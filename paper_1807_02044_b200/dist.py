@@ -71,6 +71,34 @@ def compute_banded(compute_rows: Callable, H: int, W: int, rank: int, world: int
     return res
 
 
+_SYMM = {}
+
+
+def compute_banded_scatter(m, left, right, H: int, W: int, rank: int, world: int, group=None):
+    """Row bands without the all-gather (NEXT-3 band scatter): every rank's final-map
+    kernel stores its band directly into all ranks' frame buffers, which live in
+    symmetric memory (torch.distributed._symmetric_memory: one [H, W] float32
+    buffer per rank, peers mapped into each GPU's address space, stores over
+    NVLink), then a symmetric-memory barrier.  Returns this rank's full map (a
+    view of its symmetric buffer, valid until the next call).  `m` is the rank's
+    FBS handle (fbs_create_band or full frame)."""
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm
+    key = (H, W, id(group))
+    if key not in _SYMM:
+        buf = symm.empty((H, W), dtype=torch.float32, device=left.device)
+        hdl = symm.rendezvous(buf, group if group is not None else dist.group.WORLD)
+        _SYMM[key] = (buf, hdl)
+    buf, hdl = _SYMM[key]
+    r0, r1 = band_range(H, rank, world)
+    hdl.barrier(channel=0)  # every rank is done reading the previous frame's map
+    if r1 > r0:
+        m.compute_rows_scatter(left, right, r0, r1, list(hdl.buffer_ptrs))
+    hdl.barrier(channel=0)  # every band has landed in every buffer
+    return buf
+
+
 def shard_frames(n_frames: int, rank: int, world: int) -> list[int]:
     """Frame indices owned by ``rank`` (frame i -> rank i mod world)."""
     return list(range(rank, n_frames, world))

@@ -104,3 +104,43 @@ def test_nccl_drange_split():
     mp.spawn(_drange_worker, args=(world, _free_port(), q), nprocs=world, join=True)
     got = q.get(timeout=60)
     assert np.mean(got.view(np.uint32) == ref.view(np.uint32)) > 0.995
+
+
+def _scatter_worker(rank, world, port, q):
+    import torch.distributed as dist
+    import stereo_synth as synth
+    import paper_1807_02044_b200 as fbs
+    from paper_1807_02044_b200 import dist as fdist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    cfg = synth.CONFIGS["mb2014"]
+    L, R = (torch.from_numpy(x).cuda() for x in synth.frame(cfg, 0))
+    r0, r1 = fdist.band_range(cfg.H, rank, world)
+    m = fbs.FBS(cfg.W, cfg.H, cfg.d_min, cfg.d_max, cfg.radius, cfg.gamma_d, cfg.gamma_r, rows=(r0, r1))
+    full = fdist.compute_banded_scatter(m, L, R, cfg.H, cfg.W, rank, world)
+    torch.cuda.synchronize()
+    q.put((rank, full.cpu().numpy().copy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_symmetric_memory_band_scatter():
+    """NEXT-3 band scatter over NVLink: every rank's map assembled by peer stores
+    into symmetric memory equals the single-GPU map bit for bit, on every rank."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs for symmetric memory over NVLink")
+    import torch.multiprocessing as mp
+    import stereo_synth as synth
+    import paper_1807_02044_b200 as fbs
+    world = min(8, torch.cuda.device_count())
+    cfg = synth.CONFIGS["mb2014"]
+    L, R = (torch.from_numpy(x).cuda() for x in synth.frame(cfg, 0))
+    ref = fbs.FBS(cfg.W, cfg.H, cfg.d_min, cfg.d_max, cfg.radius, cfg.gamma_d, cfg.gamma_r).compute(L, R).cpu().numpy()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.spawn(_scatter_worker, args=(world, _free_port(), q), nprocs=world, join=True)
+    for _ in range(world):
+        _, got = q.get(timeout=120)
+        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))

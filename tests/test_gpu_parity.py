@@ -457,3 +457,26 @@ def test_sparse_search_range_matches_oracle(fbs, oracle_lib, cfgname, margin):
     full = m.compute_ranged(Ld, Rd, fr, fr).cpu().numpy()
     assert np.array_equal(full.view(np.uint32), seed.cpu().numpy().view(np.uint32))
     log_errors(f"sparse-range-{cfgname}", agree=float(same.mean()), pixels=W * H)
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_rows_scatter(fbs, path):
+    """NEXT-3 band scatter: fbs_compute_rows_scatter stores rows [r0, r1) into every
+    destination frame buffer (here three on this GPU; peers' symmetric-memory
+    buffers on a multi-GPU box), bit-identical to fbs_compute, other rows untouched."""
+    cfg = synth.CONFIGS["teddy"]
+    L, R = (to_dev(x) for x in synth.frame(cfg, 0))
+    m = fbs.FBS(cfg.W, cfg.H, cfg.d_min, cfg.d_max, cfg.radius, cfg.gamma_d, cfg.gamma_r, path=path)
+    ref = m.compute(L, R).cpu().numpy()
+    bufs = [torch.full((cfg.H, cfg.W), 123.0, device="cuda") for _ in range(3)]
+    stitched = torch.full((cfg.H, cfg.W), 123.0, device="cuda")
+    edges = [0, 100, 101, 250, cfg.H]
+    for a, b in zip(edges[:-1], edges[1:]):
+        m.compute_rows_scatter(L, R, a, b, [t.data_ptr() for t in bufs] + [stitched.data_ptr()])
+    for t in bufs + [stitched]:
+        assert np.array_equal(t.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+    part = torch.full((cfg.H, cfg.W), 123.0, device="cuda")
+    m.compute_rows_scatter(L, R, 100, 180, [part.data_ptr()])
+    got = part.cpu().numpy()
+    assert np.array_equal(got[100:180].view(np.uint32), ref[100:180].view(np.uint32))
+    assert np.all(got[:100] == 123.0) and np.all(got[180:] == 123.0)
