@@ -205,6 +205,8 @@ def run_ours(args, cfg, rank, world, local_rank):
             m.compute_ranged(L, R, rl, rr, out=out)
         elif B > 1:
             m.compute_batch(Lb[i % nb], Rb[i % nb], out=outb)
+        elif banded and args.band_scatter and world > 1:  # NEXT-3: peer stores into symmetric memory
+            fdist.compute_banded_scatter(m, L, R, cfg.H, cfg.W, rank, world)
         elif banded:
             fdist.compute_banded(lambda r0, r1, band: m.compute_rows(L, R, r0, r1, out=band[: r1 - r0]),
                                  cfg.H, cfg.W, rank, world, device=dev)
@@ -448,6 +450,9 @@ def main():
     ap.add_argument("--sparse-margin", type=int, default=None,
                     help="NEXT-4: per step, suggest ranges (margin M) from the frame's full-range map "
                          "and run the ranged WTA (sparse search range)")
+    ap.add_argument("--band-scatter", action="store_true",
+                    help="mb2014 at N > 1: bands stored into the peers' symmetric-memory buffers (NEXT-3) "
+                         "instead of the NCCL all-gather")
     ap.add_argument("--no-graph", action="store_true",
                     help="time eager launches instead of CUDA-graph replays")
     ap.add_argument("--no-extras", action="store_true",
