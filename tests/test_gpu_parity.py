@@ -480,3 +480,26 @@ def test_rows_scatter(fbs, path):
     got = part.cpu().numpy()
     assert np.array_equal(got[100:180].view(np.uint32), ref[100:180].view(np.uint32))
     assert np.all(got[:100] == 123.0) and np.all(got[180:] == 123.0)
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_random_configs(fbs, oracle_lib, path):
+    """Randomised configurations against the oracle: sizes 20..140 x 12..90 (ragged
+    against every tile), disparity ranges 2..150 wide with offsets, radii 0..max,
+    gamma pairs drawn inside the accepted region (R#13), scene kinds mixed."""
+    rng = np.random.default_rng(77 if path == "volume" else 78)
+    max_r = fbs.FBS_MAX_RADIUS if path == "volume" else fbs.FBS_FUSED_MAX_RADIUS
+    n = 0
+    while n < 14:
+        W, H = int(rng.integers(20, 141)), int(rng.integers(12, 91))
+        rho = int(rng.integers(0, max_r + 1))
+        d_min = int(rng.integers(0, 20))
+        d_max = d_min + int(rng.integers(1, 150))
+        gd, gr = float(rng.uniform(1.0, 8.0)), float(rng.uniform(20.0, 200.0))
+        if rho > 0 and 1.4426950408889634 * (2 * rho * rho / gd ** 2 + 65025 / gr ** 2) > 124:
+            continue  # outside the accepted weight range (fbs_create rejects it)
+        kind = ["layered", "half", "flat", "dot5"][n % 4]
+        L, R = make_pair(kind, W, H, d_min, d_max, 1000 + n)
+        _full_check(fbs, oracle_lib, L, R, d_min, d_max, rho, gd, gr,
+                    f"random{n} {W}x{H} d={d_min}..{d_max} rho={rho} {kind}", path)
+        n += 1
