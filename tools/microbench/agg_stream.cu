@@ -4,8 +4,8 @@
 // no classification.
 #include <cstdio>
 #include <cuda_runtime.h>
-#include "../../paper_1807_02044_b200/csrc/fbs_kernels.cuh"
-using namespace fbs;
+#include "../../paper_1807_02044_b200/csrc/fbs_volume.cuh"
+using namespace fbs::vol;
 
 template <int R>
 __global__ void __launch_bounds__(256, 2) k_stream(const float* vol, size_t rowstride, int reps, float* out) {
