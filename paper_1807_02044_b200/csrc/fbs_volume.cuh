@@ -14,6 +14,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "fbs_kernels.cuh"  // fbs::OutSet (band scatter)
+
 namespace fbs {
 namespace vol {
 
