@@ -35,6 +35,9 @@ import stereo_synth as synth  # noqa: E402
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary.json")
 NOMINAL_FP32_LANES_PER_SM = 128  # B200: 4 SMSP x 32 FP32 lanes (B200_PROFILING.md: 148 SMs)
+# measured register-only FFMA2 (broadcast scalar operand) throughput on this pool's B200s
+# (tools/microbench/ffma_peak.cu, profiles/r01_ffma_microbench.txt): the practical ceiling
+FFMA2_CEILING_TFLOPS = 66.9
 
 
 def log(*a):
@@ -353,6 +356,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             "frames_per_launch": fpe,
             "peak_source": f"148 SM x 128 FP32 lanes x 2 x {peak_src} (nominal); "
                            "FFMA2 microbenchmark 66.9 TFLOP/s (DESIGN.md §6)",
+            "frac_of_ffma2_ceiling": round(achieved / FFMA2_CEILING_TFLOPS, 4),
             "useful_work": "numerator FMAs of Eq.(6): 2 sides x W*H*D*(2rho+1)^2 per launch",
             "denominator_forms": {k: round(v / max(1, sum(tiles.values())), 4) for k, v in tiles.items()}}
     base = None
