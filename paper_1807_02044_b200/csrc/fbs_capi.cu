@@ -54,6 +54,7 @@ struct fbs_ctx {
   int arows;           // rows of aggL
   float *volL, *volR, *gpadL, *gpadR, *aggL;
   uint32_t *vbitsL, *vbitsR;
+  int* rtiles;  // fbs_suggest_ranges: (min, max) per 16x16 tile, left then right
   // host path (fbs_compute_host[_batch]): two frame slots each, created on first use
   bool staging_ready;
   uint8_t *hL, *hR;
@@ -184,7 +185,7 @@ static void free_all(fbs_ctx* h) {
   free_host_path(h);
   void* ptrs[] = {h->P[0], h->P[1], h->SR[0], h->SR[1], h->G[0], h->G[1], h->bits[0], h->bits[1],
                   h->dmap[0], h->dmap[1], h->agg3, h->keys, h->tile_stats, h->trace,
-                  h->volL, h->volR, h->gpadL, h->gpadR, h->aggL, h->vbitsL, h->vbitsR};
+                  h->volL, h->volR, h->gpadL, h->gpadR, h->aggL, h->vbitsL, h->vbitsR, h->rtiles};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -410,6 +411,10 @@ static fbs_ctx* create_volume(fbs_ctx* h) {
   if (h->nblk > 1) ok &= cudaMalloc(&h->aggL, (size_t)h->arows * W * h->nblk * kDB * sizeof(float)) == cudaSuccess;
   ok &= cudaMalloc(&h->agg3, npix * sizeof(float4)) == cudaSuccess;
   ok &= cudaMalloc(&h->tile_stats, 4 * sizeof(unsigned long long)) == cudaSuccess;
+  {
+    const int T = vol::kRangeTile;
+    ok &= cudaMalloc(&h->rtiles, 4 * (size_t)((W + T - 1) / T) * ((H + T - 1) / T) * sizeof(int)) == cudaSuccess;
+  }
 #ifdef FBS_TRACE
   ok &= cudaMalloc(&h->trace, 8192 * sizeof(unsigned long long)) == cudaSuccess;
 #endif
@@ -963,16 +968,15 @@ extern "C" int fbs_suggest_ranges(fbs_ctx* h, const float* seed_disp, int margin
                                   int16_t* ranges_r, fbs_stream_t stream) {
   if (!h || !seed_disp || !ranges_l || !ranges_r) return fail(FBS_E_ARG, "fbs_suggest_ranges: NULL argument");
   if (margin < 0) return fail(FBS_E_PARAM, "fbs_suggest_ranges: margin must be >= 0");
+  if (h->path != FBS_PATH_VOLUME) return fail(FBS_E_UNSUPPORTED, "fbs_suggest_ranges: volume path only");
   cudaStream_t s = (cudaStream_t)stream;
   const int W = h->W, H = h->H, T = vol::kRangeTile;
   const int tx = (W + T - 1) / T, ty = (H + T - 1) / T, n = 2 * tx * ty;
-  int* tiles = nullptr;  // (min, max) per tile, left then right
-  if (cudaMallocAsync(&tiles, 2 * n * sizeof(int), s) != cudaSuccess) return fail(FBS_E_OOM, "fbs_suggest_ranges");
+  int* tiles = h->rtiles;  // (min, max) per tile, left then right (allocated in fbs_create)
   vol::k_range_init<<<(2 * n + 255) / 256, 256, 0, s>>>(tiles, 2 * n);
   vol::k_range_seeds<<<dim3((W + 127) / 128, H), 128, 0, s>>>(seed_disp, W, H, tx, tiles, tiles + n);
   vol::k_range_expand<<<dim3((W + 127) / 128, H), 128, 0, s>>>(tiles, tiles + n, W, H, tx, h->d_min, h->d_max, margin,
                                                               (short2*)ranges_l, (short2*)ranges_r);
-  cudaFreeAsync(tiles, s);
   return cuda_check(cudaGetLastError(), "fbs_suggest_ranges");
 }
 
