@@ -27,6 +27,19 @@
 #include "fbs_ws.cuh"
 #include "fbs_volume.cuh"
 
+// Radii instantiated per kernel family.  FBS_EXP_ONLY_R4 (experiment builds of
+// tools/build_variants.py only) compiles radius 4 alone; other radii then fail
+// with cudaErrorInvalidValue at launch.
+#ifdef FBS_EXP_ONLY_R4
+#define FBS_VOL_RADII(M) M(4)
+#define FBS_WS_RADII(M) M(4)
+#define FBS_SYNC_RADII(M)
+#else
+#define FBS_VOL_RADII(M) M(0) M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8) M(9) M(10)
+#define FBS_WS_RADII(M) M(0) M(1) M(2) M(3) M(4)
+#define FBS_SYNC_RADII(M) M(5) M(6)
+#endif
+
 using namespace fbs;
 
 struct fbs_ctx {
@@ -353,8 +366,7 @@ static fbs_ctx* create_impl(int W, int H, int d_min, int d_max, int radius, floa
     cudaFuncSetAttribute(k_fbs<RR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
     cudaFuncSetAttribute(k_fbs<RR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
     break;
-    FBS_SMEM_WS(0) FBS_SMEM_WS(1) FBS_SMEM_WS(2) FBS_SMEM_WS(3) FBS_SMEM_WS(4) FBS_SMEM_ATTR(5)
-    FBS_SMEM_ATTR(6)
+    FBS_WS_RADII(FBS_SMEM_WS) FBS_SYNC_RADII(FBS_SMEM_ATTR)
 #undef FBS_SMEM_ATTR
 #undef FBS_SMEM_WS
   }
@@ -451,8 +463,7 @@ static fbs_ctx* create_volume(fbs_ctx* h) {
                        sizeof(vol::AggSmem<RR>));                                                             \
   cudaFuncSetAttribute(vol::k_agg<RR, false, false, false, true>,                                             \
                        cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(vol::AggSmem<RR>));
-  FBS_SMEM_ATTR(0) FBS_SMEM_ATTR(1) FBS_SMEM_ATTR(2) FBS_SMEM_ATTR(3) FBS_SMEM_ATTR(4)
-  FBS_SMEM_ATTR(5) FBS_SMEM_ATTR(6) FBS_SMEM_ATTR(7) FBS_SMEM_ATTR(8) FBS_SMEM_ATTR(9) FBS_SMEM_ATTR(10)
+  FBS_VOL_RADII(FBS_SMEM_ATTR)
 #undef FBS_SMEM_ATTR
   cudaFuncSetAttribute(vol::k_cost, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)vol::cost_smem_bytes(4096 / kDB));
@@ -514,7 +525,7 @@ static cudaError_t launch_walk(const fbs_ctx* h, const WalkArgs& a, bool exp, cu
   case RR:                                                                                                \
     return exp ? launch_pdl(k_fbs<RR, true>, grid, block, smem, s, a)                                     \
                : launch_pdl(k_fbs<RR, false>, grid, block, smem, s, a);
-    FBS_CASE_WS(0) FBS_CASE_WS(1) FBS_CASE_WS(2) FBS_CASE_WS(3) FBS_CASE_WS(4) FBS_CASE(5) FBS_CASE(6)
+    FBS_WS_RADII(FBS_CASE_WS) FBS_SYNC_RADII(FBS_CASE)
 #undef FBS_CASE
 #undef FBS_CASE_WS
   }
@@ -603,8 +614,7 @@ static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0,
                  : launch_pdl(vol::k_agg<RR, kVolEmpty, false>, grid, dim3(vol::AggGeom<RR>::THREADS),        \
                               sizeof(vol::AggSmem<RR>), s, a);                                                \
     break;
-      FBS_CASE(0) FBS_CASE(1) FBS_CASE(2) FBS_CASE(3) FBS_CASE(4) FBS_CASE(5) FBS_CASE(6)
-      FBS_CASE(7) FBS_CASE(8) FBS_CASE(9) FBS_CASE(10)
+      FBS_VOL_RADII(FBS_CASE)
 #undef FBS_CASE
     }
     if (e != cudaSuccess) return cuda_check(e, "k_agg launch");
