@@ -5,6 +5,9 @@
 //   mode 2: LDS.64,  one address for the whole warp
 //   mode 3: LDS.64,  one address per half-warp
 //   mode 4: LDS.32,  one address per half-warp
+//   mode 5: LDS.128, one address per quarter-warp (four distinct, disjoint banks)
+//   mode 6: LDS.128, one address per quarter-warp (four distinct, same banks)
+//   mode 7: LDS.128, one address per eighth-warp (eight distinct, disjoint banks)
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o lds_wavefronts lds_wavefronts.cu
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -24,6 +27,9 @@ __global__ void k_lds(float* out, int iters) {
     if (MODE == 2) { float2 v = *reinterpret_cast<float2*>(&s[base]); acc += v.x + v.y; }
     if (MODE == 3) { float2 v = *reinterpret_cast<float2*>(&s[base + 2 * half + 32 * half]); acc += v.x + v.y; }
     if (MODE == 4) { acc += s[base + half * 33]; }
+    if (MODE == 5) { float4 v = *reinterpret_cast<float4*>(&s[base + 4 * (lane >> 3)]); acc += v.x + v.y + v.z + v.w; }
+    if (MODE == 6) { float4 v = *reinterpret_cast<float4*>(&s[base + 32 * (lane >> 3)]); acc += v.x + v.y + v.z + v.w; }
+    if (MODE == 7) { float4 v = *reinterpret_cast<float4*>(&s[base + 4 * (lane >> 2)]); acc += v.x + v.y + v.z + v.w; }
   }
   out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
@@ -36,6 +42,9 @@ int main() {
   k_lds<2><<<148, 256>>>(out, 1024);
   k_lds<3><<<148, 256>>>(out, 1024);
   k_lds<4><<<148, 256>>>(out, 1024);
+  k_lds<5><<<148, 256>>>(out, 1024);
+  k_lds<6><<<148, 256>>>(out, 1024);
+  k_lds<7><<<148, 256>>>(out, 1024);
   printf("done %d\n", (int)cudaDeviceSynchronize());
   return 0;
 }
