@@ -32,12 +32,10 @@
 // with cudaErrorInvalidValue at launch.
 #ifdef FBS_EXP_ONLY_R4
 #define FBS_VOL_RADII(M) M(4)
-#define FBS_AGG8_RADII(M) M(4)
 #define FBS_WS_RADII(M) M(4)
 #define FBS_SYNC_RADII(M)
 #else
 #define FBS_VOL_RADII(M) M(0) M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8) M(9) M(10)
-#define FBS_AGG8_RADII(M) M(1) M(2) M(3) M(4)
 #define FBS_WS_RADII(M) M(0) M(1) M(2) M(3) M(4)
 #define FBS_SYNC_RADII(M) M(5) M(6)
 #endif
@@ -399,7 +397,7 @@ static fbs_ctx* create_volume(fbs_ctx* h) {
   const int W = h->W, H = h->H, R = h->R;
   h->fcap = 1;
   h->TX = vol::kTX;
-  h->TY = vol::agg8_radius(R) ? vol::a8::kT : vol::agg_tile_h(R);  // the production kernel's tile height
+  h->TY = vol::agg_tile_h(R);
   h->Wv = (W + vol::kTX - 1) / vol::kTX * vol::kTX + 2 * R;
   {  // rows of the served band [rb0, rb1): cost rows [vbase, ..), tile rows [abase, ..)
     const int TY = h->TY, ty0 = h->rb0 / TY, ty1 = (h->rb1 + TY - 1) / TY;
@@ -467,13 +465,6 @@ static fbs_ctx* create_volume(fbs_ctx* h) {
                        cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(vol::AggSmem<RR>));
   FBS_VOL_RADII(FBS_SMEM_ATTR)
 #undef FBS_SMEM_ATTR
-#define FBS_SMEM_ATTR8(RR)                                                                                    \
-  cudaFuncSetAttribute(vol::k_agg8<RR, kVolEmpty, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
-                       sizeof(vol::Agg8Smem<RR>));                                                            \
-  cudaFuncSetAttribute(vol::k_agg8<RR, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,             \
-                       sizeof(vol::Agg8Smem<RR>));
-  FBS_AGG8_RADII(FBS_SMEM_ATTR8)
-#undef FBS_SMEM_ATTR8
   cudaFuncSetAttribute(vol::k_cost, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)vol::cost_smem_bytes(4096 / kDB));
   if (cuda_check(cudaGetLastError(), "fbs_create smem attributes") != FBS_OK) {
@@ -557,10 +548,7 @@ static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0,
   // aggregation tiles are anchored at multiples of the tile height in frame rows, so a
   // pixel's denominator form never depends on the band; cost rows cover the
   // tiles' windows (the classification reads validity masks over them too)
-  // k_agg8 (radii 1..4) is the production kernel and also exports; the disparity-range
-  // split and the sparse search range run k_agg's KEYS / RANGED instantiations
-  const bool use8 = vol::agg8_radius(R) && !kq && !ranges;
-  const int TY = use8 ? vol::a8::kT : vol::agg_tile_h(R);
+  const int TY = vol::agg_tile_h(R);
   const int ty0 = r0 / TY, ty1 = (r1 + TY - 1) / TY;
   const int c0 = std::max(0, ty0 * TY - R), c1 = std::min(H, ty1 * TY + R);  // cost rows
   float* aggL_exp = expA ? expA[0] : nullptr;
@@ -612,20 +600,9 @@ static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0,
   a.ranges[0] = ranges ? ranges[0] : nullptr;
   a.ranges[1] = ranges ? ranges[1] : nullptr;
   {
-    const dim3 grid((W + vol::kTX - 1) / vol::kTX, ty1 - ty0, 2);  // 16-wide tiles for both kernels
+    const dim3 grid((W + vol::kTX - 1) / vol::kTX, ty1 - ty0, 2);
     cudaError_t e = cudaErrorInvalidValue;
-    if (use8) switch (R) {
-#define FBS_CASE8(RR)                                                                                         \
-  case RR:                                                                                                    \
-    e = aggR_exp ? launch_pdl(vol::k_agg8<RR, false, true>, grid, dim3(vol::a8::kThreads),                    \
-                              sizeof(vol::Agg8Smem<RR>), s, a)                                                \
-                 : launch_pdl(vol::k_agg8<RR, kVolEmpty, false>, grid, dim3(vol::a8::kThreads),               \
-                              sizeof(vol::Agg8Smem<RR>), s, a);                                               \
-    break;
-      FBS_AGG8_RADII(FBS_CASE8)
-#undef FBS_CASE8
-    }
-    else switch (R) {
+    switch (R) {
 #define FBS_CASE(RR)                                                                                          \
   case RR:                                                                                                    \
     e = aggR_exp ? launch_pdl(vol::k_agg<RR, false, true>, grid, dim3(vol::AggGeom<RR>::THREADS),             \

@@ -54,7 +54,7 @@ struct AggGeom {
   static constexpr bool kRolled = R >= 7;         // cost-row loop instead of the unrolled stream
   static constexpr int CWS = R >= 7 ? 96 : 64;    // classification words per warp (PY + 2R <= 24 rows x 4)
 };
-constexpr int kTYMax = 16;                        // tallest CTA tile of any radius (k_agg8, fbs_agg8.cuh)
+constexpr int kTYMax = kPYMax * 2;                // tallest CTA tile of any radius
 __host__ __device__ constexpr int agg_tile_h(int R) { return R >= 7 ? 4 : (R >= 6 ? 4 : kPYMax) * 2; }
 
 #ifndef FBS_KCX
@@ -1073,8 +1073,6 @@ __global__ void k_select_wta(const float* __restrict__ agg, int W, int H, int D,
   }
   disp[p] = best > kSent ? d_min + bi : -1;
 }
-
-#include "fbs_agg8.cuh"  // k_agg8: radii 1..4
 
 }  // namespace vol
 }  // namespace fbs

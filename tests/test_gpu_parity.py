@@ -110,17 +110,12 @@ def test_volumes_and_maps(fbs, oracle_lib, case, path):
     # fbs_compute gives the same bytes as the debug path
     out2 = m.compute(Ld, Rd).cpu().numpy()
     assert np.array_equal(out2.view(np.uint32), out.view(np.uint32))
-    if name in ("textureless", "teddy"):  # together they exercise every denominator form
+    if name == "textureless":  # exercises every denominator form
         m.profile_enable(1)
         out3 = m.compute(Ld, Rd).cpu().numpy()
         forms = m.tile_stats()
         m.profile_enable(0)
-        if name == "textureless":  # EDGE, GENERAL and EMPTY units (and FAST on the fused
-            # path, whose units are smaller than the volume path's 8x8 k_agg8 warp tiles)
-            need = ("edge", "general", "empty") + (("fast",) if path == "fused" else ())
-            assert all(forms[k] > 0 for k in need), forms
-        else:  # a textured frame: mostly FAST units
-            assert forms["fast"] > 0, forms
+        assert min(forms.values()) > 0, forms  # both paths have all four denominator forms
         assert np.array_equal(out3.view(np.uint32), out.view(np.uint32))
     # every disagreement was checked to be an oracle near-tie (gap < 1e-5); scenes
     # with textureless layers have many exact ties (perfect correlations at
