@@ -420,8 +420,7 @@ static fbs_ctx* create_volume(fbs_ctx* h) {
   ok &= cudaMalloc(&h->volR, nvol * 4) == cudaSuccess;
   ok &= cudaMalloc(&h->dmap[0], npix * 4) == cudaSuccess;
   ok &= cudaMalloc(&h->dmap[1], npix * 4) == cudaSuccess;
-  // no left aggregated volume: one-d-block frames keep it on chip, several d-blocks carry
-  // the Eq.(10) record across blocks (k_agg REC); only the debug export stores it (temporary)
+  if (h->nblk > 1) ok &= cudaMalloc(&h->aggL, (size_t)h->arows * W * h->nblk * kDB * sizeof(float)) == cudaSuccess;
   ok &= cudaMalloc(&h->agg3, npix * sizeof(float4)) == cudaSuccess;
   ok &= cudaMalloc(&h->tile_stats, 4 * sizeof(unsigned long long)) == cudaSuccess;
   {
@@ -460,12 +459,10 @@ static fbs_ctx* create_volume(fbs_ctx* h) {
                        sizeof(vol::AggSmem<RR>));                                                             \
   cudaFuncSetAttribute(vol::k_agg<RR, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
                        sizeof(vol::AggSmem<RR>));                                                             \
-  cudaFuncSetAttribute(vol::k_agg<RR, false, false, true, false, true>,                                       \
-                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vol::agg_smem_bytes<RR, true>());    \
-  cudaFuncSetAttribute(vol::k_agg<RR, false, false, false, true, true>,                                       \
-                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vol::agg_smem_bytes<RR, true>());    \
-  cudaFuncSetAttribute(vol::k_agg<RR, kVolEmpty, false, false, false, true>,                                  \
-                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vol::agg_smem_bytes<RR, true>());
+  cudaFuncSetAttribute(vol::k_agg<RR, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                       sizeof(vol::AggSmem<RR>));                                                             \
+  cudaFuncSetAttribute(vol::k_agg<RR, false, false, false, true>,                                             \
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(vol::AggSmem<RR>));
   FBS_VOL_RADII(FBS_SMEM_ATTR)
 #undef FBS_SMEM_ATTR
   cudaFuncSetAttribute(vol::k_cost, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -588,15 +585,13 @@ static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0,
   // one d-block: the left costs stay on chip and only Eq.(10)'s three are stored
   // (unless the debug export wants the whole left volume)
   float* aggL_tmp = nullptr;
-  if (aggL_exp && !h->aggL) {  // debug export of the left volume: temporary full store
-    if (cudaMalloc(&aggL_tmp, (size_t)W * H * h->nblk * kDB * sizeof(float)) != cudaSuccess)
+  if (aggL_exp && !h->aggL) {  // single-block frame exporting its left volume: temporary store
+    if (cudaMalloc(&aggL_tmp, (size_t)W * H * kDB * sizeof(float)) != cudaSuccess)
       return fail(FBS_E_OOM, "fbs_debug_volumes: scratch");
     a.aggL = aggL_tmp;
     a.abase = 0;
   }
   a.agg3 = (h->nblk == 1 && !aggL_exp) ? h->agg3 : nullptr;
-  a.rec = (h->nblk > 1 && !aggL_exp) ? h->agg3 : nullptr;  // same [H][W] float4 records
-  const float4* rec3 = a.agg3 ? a.agg3 : a.rec;
   a.tile_stats = ev ? h->tile_stats : nullptr;
   a.c_lo = kq ? kq->c_lo : 0;
   a.c_hi = kq ? kq->c_hi : h->D - 1;
@@ -612,12 +607,10 @@ static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0,
   case RR:                                                                                                    \
     e = aggR_exp ? launch_pdl(vol::k_agg<RR, false, true>, grid, dim3(vol::AggGeom<RR>::THREADS),             \
                               sizeof(vol::AggSmem<RR>), s, a)                                                 \
-        : kq     ? launch_pdl(vol::k_agg<RR, false, false, true, false, true>, grid,                          \
-                              dim3(vol::AggGeom<RR>::THREADS), vol::agg_smem_bytes<RR, true>(), s, a)         \
-        : ranges ? launch_pdl(vol::k_agg<RR, false, false, false, true, true>, grid,                          \
-                              dim3(vol::AggGeom<RR>::THREADS), vol::agg_smem_bytes<RR, true>(), s, a)         \
-        : a.rec  ? launch_pdl(vol::k_agg<RR, kVolEmpty, false, false, false, true>, grid,                     \
-                              dim3(vol::AggGeom<RR>::THREADS), vol::agg_smem_bytes<RR, true>(), s, a)         \
+        : kq     ? launch_pdl(vol::k_agg<RR, false, false, true>, grid, dim3(vol::AggGeom<RR>::THREADS),      \
+                              sizeof(vol::AggSmem<RR>), s, a)                                                 \
+        : ranges ? launch_pdl(vol::k_agg<RR, false, false, false, true>, grid,                                \
+                              dim3(vol::AggGeom<RR>::THREADS), sizeof(vol::AggSmem<RR>), s, a)                \
                  : launch_pdl(vol::k_agg<RR, kVolEmpty, false>, grid, dim3(vol::AggGeom<RR>::THREADS),        \
                               sizeof(vol::AggSmem<RR>), s, a);                                                \
     break;
@@ -630,7 +623,7 @@ static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0,
   if (ev) cudaEventRecord(ev[2], s);
   if (kq) {  // disparity-range split: the records instead of the final map
     const dim3 grd((W + 127) / 128, r1 - r0);
-    vol::k_records<<<grd, 128, 0, s>>>(h->dmap[0], a.aggL, rec3, h->nblk, W, r0, r1, h->d_min, h->d_max, a.abase,
+    vol::k_records<<<grd, 128, 0, s>>>(h->dmap[0], a.aggL, a.agg3, h->nblk, W, r0, r1, h->d_min, h->d_max, a.abase,
                                        kq->rec_l);
     h->launches += 1;
     if (ev) cudaEventRecord(ev[3], s);
@@ -640,7 +633,7 @@ static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0,
     const dim3 grd((W + 127) / 128, r1 - r0);
     const cudaError_t e = launch_pdl(h->scat.n ? vol::k_finalize<true> : vol::k_finalize<false>, grd, dim3(128), 0,
                                      s, (const int32_t*)h->dmap[0],
-                                     (const int32_t*)h->dmap[1], (const float*)a.aggL, rec3,
+                                     (const int32_t*)h->dmap[1], (const float*)a.aggL, (const float4*)a.agg3,
                                      h->nblk, W, r0, r1, h->d_min, h->d_max, a.abase, out,
                                      (const short2*)(ranges ? ranges[0] : nullptr), h->scat);
     if (e != cudaSuccess) return cuda_check(e, "k_finalize launch");

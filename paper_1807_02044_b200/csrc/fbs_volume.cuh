@@ -437,8 +437,6 @@ struct AggArgs {
   float* aggL;                   // left aggregated costs, [H][nblk][W][64] (read by k_finalize)
   float4* agg3;                  // if set (one d-block, no export): only (c(d*-1), c(d*), c(d*+1)) per
                                  // left pixel, [H][W] float4, instead of aggL
-  float4* rec;                   // if set (several d-blocks, no export; REC instantiations): the same
-                                 // record, tracked across d-blocks in registers, instead of aggL
   float* exportR;                // optional [H][W][D] right aggregated volume (debug)
   // KEYS instantiation (disparity-range split, NEXT-3): only local disparity indices
   // [c_lo, c_hi] compete in the WTA; the per-pixel keys (global d) are written out
@@ -488,17 +486,6 @@ struct AggSmem {
   short2 rng[AggGeom<R>::TY][kTX];                  // RANGED: the tile's per-pixel suggested ranges
   int rlo, rhi;                                     // RANGED: their union
 };
-
-// REC instantiations only (appended after AggSmem<R>): per (warp, half, slot)
-template <int R>
-struct AggRec {
-  static constexpr int NW = AggGeom<R>::NW, SL = kPX * AggGeom<R>::HPY;
-  float2 rnb[NW][2][SL][16];  // (c(d-1), c(d+1)) of lane dq's lane-local winner of slot s
-  float rlast[NW][2][32];     // c(last d of a d-block), double-buffered by block parity
-  float rfirst[NW][32];       // c(first d of this d-block)
-};
-template <int R, bool REC>
-constexpr size_t agg_smem_bytes() { return sizeof(AggSmem<R>) + (REC ? sizeof(AggRec<R>) : 0); }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -756,13 +743,6 @@ __device__ __forceinline__ unsigned long long wta_butterfly16(unsigned long long
   return k[0];
 }
 
-// c(d+1) not known yet: d is the last disparity of its d-block (a NaN payload no cost takes)
-constexpr unsigned kNextMark = 0x7fc0beefu;
-// inverse of fkey
-__device__ __forceinline__ float fkey_inv(unsigned u) {
-  return __uint_as_float((u & 0x80000000u) ? (u ^ 0x80000000u) : ~u);
-}
-
 // grid: (ceil(W/kTX), tile rows, 2 sides); block AggGeom<R>::THREADS (warps of 4 x PY sub-tiles).
 // EMPTY: whether GENERAL units test for the EMPTY special case (the production
 // instantiation does: KITTI +22.5 %, Teddy -0.6 %).  Bit-identical
@@ -771,20 +751,13 @@ __device__ __forceinline__ float fkey_inv(unsigned u) {
 // store loop alone costs the production kernel ~1 %).
 // KEYS: disparity-range split (fbs_compute_keys); RANGED: sparse search range
 // (fbs_compute_ranged).
-// REC: frames with several d-blocks keep no left aggregated volume: each lane leaves
-// in shared memory, for its lane-local winner of every slot, the costs at d-1 and d+1
-// (neighbour lanes by shuffle, d-block ends through shared memory); after the WTA
-// butterfly the slot owner reads them from the winning lane and tracks the running
-// record (c(d*-1), c(d*), c(d*+1)) across d-blocks (Eq.(10) needs nothing else,
-// P:L167-170).
-template <int R, bool EMPTY, bool EXPORT, bool KEYS = false, bool RANGED = false, bool REC = false>
+template <int R, bool EMPTY, bool EXPORT, bool KEYS = false, bool RANGED = false>
 __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(const AggArgs a) {
   constexpr int kPY = AggGeom<R>::PY;
   constexpr int kTY = AggGeom<R>::TY;
   constexpr int kThreads = AggGeom<R>::THREADS;
   extern __shared__ __align__(16) unsigned char smraw[];
   AggSmem<R>& sm = *reinterpret_cast<AggSmem<R>*>(smraw);
-  AggRec<R>& rs = *reinterpret_cast<AggRec<R>*>(smraw + sizeof(AggSmem<R>));  // REC only
   constexpr int K1 = 2 * R + 1;
   constexpr int GW = AggSmem<R>::GW, GH = AggSmem<R>::GH, GWS = AggSmem<R>::GWS;
   const int side = blockIdx.z;  // 0: left volume / left guide, 1: right
@@ -910,9 +883,6 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
     return AggSmem<R>::kAlias ? sm.w[warp] + (py0 + pyl) * RS : sm.val[warp] + (py0 + pyl) * kPX * kDB;
   };
   unsigned long long best = 0ull;  // running best key of slot (lane & 15) of this half
-  const bool recm = REC && side == 0 && a.rec != nullptr;  // warp-uniform
-  float rcm = kSent, rcp = kSent;  // REC: record neighbours of the running best
-  bool rpend = false;              // REC: c(d*+1) lies in the next d-block
   for (int b = b_lo; b <= b_hi; ++b) {
     // volume row (sy + py0 - R + r) + R = sy + py0 + r; column (sx - R + j) + R = sx + j
     const float* vb = vol + vol_at(sy + py0 - a.vbase, b, sx, a.nblk, a.Wv) + 4 * dq;
@@ -963,22 +933,10 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
       const bool h = b23 > b01;
       const int t = h ? 2 + h23 : h01;
       k[pyl * kPX + px] = ((unsigned long long)fkey(h ? b23 : b01) << 32) | (unsigned)(0xffff - (di0 + t));
-      if constexpr (REC) {
-        if (recm) {  // raw costs at d-1, d+1 of the lane-local winner (range rules at the end)
-          const int s = pyl * kPX + px;
-          const float uw = __shfl_up_sync(0xffffffffu, agg.w, 1), dx1 = __shfl_down_sync(0xffffffffu, agg.x, 1);
-          const float prevl = b > b_lo ? rs.rlast[warp][(b - 1) & 1][half * 16 + s] : kSent;
-          const float cm = t == 0 ? (dq == 0 ? prevl : uw) : (t == 1 ? agg.x : (t == 2 ? agg.y : agg.z));
-          const float cp = t == 3 ? (dq == 15 ? __uint_as_float(kNextMark) : dx1) : (t == 0 ? agg.y : (t == 1 ? agg.z : agg.w));
-          rs.rnb[warp][half][s][dq] = make_float2(cm, cp);
-          if (dq == 15) rs.rlast[warp][b & 1][half * 16 + s] = agg.w;
-          if (dq == 0) rs.rfirst[warp][half * 16 + s] = agg.x;
-        }
-      }
       if (side == 0) {
         if (a.agg3)  // its weight row is dead: the stream of half-row pyl is done
           *reinterpret_cast<float4*>(vrow(pyl) + px * kDB + 4 * dq) = agg;
-        else if (!recm && x < a.W && y < a.H)
+        else if (x < a.W && y < a.H)
           *reinterpret_cast<float4*>(a.aggL + (((size_t)(y - a.abase) * a.nblk + b) * a.W + x) * kDB + 4 * dq) = agg;
       } else if ((EXPORT ? a.exportR : nullptr) && x < a.W && y >= a.r0 && y < a.r1) {
         float* er = (EXPORT ? a.exportR : nullptr) + ((size_t)y * a.W + x) * a.D;
@@ -1026,12 +984,7 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
       // every aggregated cost of the unit is SENT, which never wins the WTA (an
       // all-SENT pixel stays INVALID whatever key it keeps): only the full left
       // store and the debug export need the values
-      if (recm) {  // the d-block ends are SENT too
-        if (dq == 15)
-          for (int s2 = 0; s2 < 16; ++s2) rs.rlast[warp][b & 1][half * 16 + s2] = kSent;
-        if (dq == 0)
-          for (int s2 = 0; s2 < 16; ++s2) rs.rfirst[warp][half * 16 + s2] = kSent;
-      } else if (side == 0 && !a.agg3) {
+      if (side == 0 && !a.agg3) {
 #pragma unroll 1
         for (int s2 = 0; s2 < kPX * HPY; ++s2) {
           const int y = sy + py0 + s2 / kPX, x = sx + s2 % kPX;
@@ -1068,26 +1021,6 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
         }
       }
     }
-    if constexpr (REC) {
-      if (recm) {
-        const unsigned long long kb = wta_butterfly16(k, lane);
-        __syncwarp();  // rnb / rfirst of this d-block
-        const int sl = lane & 15;
-        if (rpend) {   // the running best sat on the previous d-block's last disparity
-          rcp = rs.rfirst[warp][half * 16 + sl];
-          rpend = false;
-        }
-        if (kb > best) {  // earlier blocks win ties (smaller d); kb > 0: a real key of this block
-          best = kb;
-          const int dl = (0xffff - (int)(kb & 0xffffu)) - b * kDB;  // winner's index within the block
-          const float2 nb = rs.rnb[warp][half][min(sl, AggRec<R>::SL - 1)][dl >> 2];
-          rcm = nb.x;
-          rcp = nb.y;
-          rpend = __float_as_uint(nb.y) == kNextMark;
-        }
-        continue;
-      }
-    }
     best = umax64(best, wta_butterfly16(k, lane));  // earlier blocks win ties (smaller d)
   }
 
@@ -1114,16 +1047,6 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
             in_p = in_p && d_int + 1 <= r.y;
           }
           a.agg3[(size_t)y * a.W + x] = make_float4(in_m ? vr[di - 1] : kSent, vr[di], in_p ? vr[di + 1] : kSent, 0.f);
-        }
-        if (REC && recm && ok) {
-          bool in_m = d_int > a.d_min, in_p = d_int < a.d_max && !rpend;
-          if constexpr (RANGED) {  // R#33
-            const short2 r = sm.rng[wy + py0 + s2 / kPX][wx + s2 % kPX];
-            in_m = in_m && d_int - 1 >= r.x;
-            in_p = in_p && d_int + 1 <= r.y;
-          }
-          a.rec[(size_t)y * a.W + x] =
-              make_float4(in_m ? rcm : kSent, fkey_inv((unsigned)(best >> 32)), in_p ? rcp : kSent, 0.f);
         }
       }
     }
