@@ -478,10 +478,25 @@ def main():
     else:
         import torch
         import torch.distributed as dist
+        # FBS_BENCH_BACKEND=gloo: a dry run of the multi-rank logic (frame sharding, row
+        # bands + gather, max-over-ranks timing) with more ranks than GPUs; the line is
+        # marked "dry_run" and is not a measurement.  The default is NCCL, one GPU per rank.
+        backend = os.environ.get("FBS_BENCH_BACKEND", "nccl")
+        dev_index = local_rank
         if world > 1:
-            torch.cuda.set_device(local_rank)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        res = run_ours(args, cfg, rank, world, local_rank)
+            if backend == "nccl":
+                torch.cuda.set_device(local_rank)
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+            else:
+                if args.band_scatter:
+                    ap.error("--band-scatter needs NCCL and one GPU per rank")
+                dev_index = local_rank % torch.cuda.device_count()
+                torch.cuda.set_device(dev_index)
+                dist.init_process_group(backend)
+        res = run_ours(args, cfg, rank, world, dev_index)
+        if res is not None and world > 1 and backend != "nccl":
+            res["dry_run"] = (f"{backend} backend, {world} ranks on {torch.cuda.device_count()} GPU(s): "
+                              "checks the multi-rank logic only, not a measurement")
         if world > 1:
             dist.destroy_process_group()
     if rank == 0 and res is not None:

@@ -62,8 +62,13 @@ def compute_banded(compute_rows: Callable, H: int, W: int, rank: int, world: int
     if r1 > r0:
         compute_rows(r0, r1, band)
     if world > 1:
-        dist.all_gather_into_tensor(full, band.contiguous() if not band.is_contiguous() else band,
-                                    group=group)
+        if full.is_cuda and dist.get_backend(group) != "nccl":  # gloo gathers host tensors
+            host = full.cpu()
+            dist.all_gather_into_tensor(host, host[rank * B:(rank + 1) * B].clone(), group=group)
+            full.copy_(host)
+        else:
+            dist.all_gather_into_tensor(full, band.contiguous() if not band.is_contiguous() else band,
+                                        group=group)
     res = full[:H]
     if out is not None:
         out.copy_(res)
