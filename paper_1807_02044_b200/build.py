@@ -11,8 +11,14 @@ SRC = [os.path.join(HERE, "csrc", "fbs_capi.cu")]
 DEPS = SRC + [os.path.join(HERE, "csrc", "fbs_kernels.cuh"), os.path.join(HERE, "csrc", "fbs_fused.cuh"), os.path.join(HERE, "csrc", "fbs_ws.cuh"), os.path.join(HERE, "csrc", "fbs_volume.cuh"), os.path.join(ROOT, "include", "fbs.h")]
 OUT = os.path.join(HERE, "libfbs.so")
 
+# Whole-module device compilation: `--split-compile` partitions the module and changes
+# the code NVVM generates for every kernel (k_agg<4>: 7,248 instructions split vs 7,000
+# whole; A/B on one B200: Teddy 6,610 -> 6,742 frames/s, KITTI +2.2 %, Tsukuba +2.7 %),
+# at ~4 min instead of ~1.5 min of build time.  FBS_SPLIT_COMPILE=1 restores the split
+# build for quick experiment builds.
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", "--split-compile=0"]
+              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"] + (
+                  ["--split-compile=0"] if os.environ.get("FBS_SPLIT_COMPILE") == "1" else [])
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

@@ -196,9 +196,9 @@ __device__ __forceinline__ void cost_side(const CostArgs& a, unsigned char* smra
       cd0[m] = (int)__dp4a(ps, SIDE == 0 ? po[m + 1] : po[m], 0u);
       cd1[m] = (int)__dp4a(ps, SIDE == 0 ? po[m] : po[m + 1], 0u);
     }
-#pragma unroll
-    for (int u = 0; u < PPW; ++u) {
-      if (u >= npx) break;
+    float* vb = vp + (size_t)b * bstride;
+    // one pixel's two values (u = pixel within the warp's run)
+    auto value2 = [&](int u) {
       const int2 ss = sSR[u];
       const float rsf = __int_as_float(ss.y);
       float o[2];
@@ -216,7 +216,17 @@ __device__ __forceinline__ void cost_side(const CostArgs& a, unsigned char* smra
       }
       if (pad0) o[0] = kUndef;  // padded disparity slots of the last block
       if (pad1) o[1] = kUndef;
-      *reinterpret_cast<float2*>(vp + (size_t)b * bstride + u * kDB) = make_float2(o[0], o[1]);
+      *reinterpret_cast<float2*>(vb + u * kDB) = make_float2(o[0], o[1]);
+    };
+    if (npx == PPW) {  // every CTA column but the frame's last: no per-pixel guard
+#pragma unroll
+      for (int u = 0; u < PPW; ++u) value2(u);
+    } else {
+#pragma unroll
+      for (int u = 0; u < PPW; ++u) {
+        if (u >= npx) break;
+        value2(u);
+      }
     }
   }
 }
