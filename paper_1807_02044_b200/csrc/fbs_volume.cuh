@@ -236,7 +236,13 @@ __host__ __device__ constexpr size_t cost_smem_bytes(int nblk) {
 }
 
 // grid: (ceil(W/kCX), r1-r0, 2 sides); block 256 = 8 warps; warp <-> pixel, lane <-> d pair.
-__global__ void __launch_bounds__(256) k_cost(CostArgs a) {
+// k_cost is issue-bound (~75 % issue active, the rest barrier / load stalls): a
+// 48-register cap puts 5 CTAs (40 warps) on an SM instead of 4 at 59 registers
+// (A/B: k_cost 30.4 -> 28.6 us at Teddy; 6 CTAs at 40 registers: 28.7 us, spills)
+#ifndef FBS_KCOST_MINB
+#define FBS_KCOST_MINB 5
+#endif
+__global__ void __launch_bounds__(256, FBS_KCOST_MINB) k_cost(CostArgs a) {
   extern __shared__ __align__(16) unsigned char csm[];
   pdl_trigger();  // k_agg may be scheduled now; it waits for our results in pdl_wait()
   if (blockIdx.z == 0) cost_side<0>(a, csm);
