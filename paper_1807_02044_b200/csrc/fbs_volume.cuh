@@ -776,9 +776,39 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
   AggSmem<R>& sm = *reinterpret_cast<AggSmem<R>*>(smraw);
   constexpr int K1 = 2 * R + 1;
   constexpr int GW = AggSmem<R>::GW, GH = AggSmem<R>::GH, GWS = AggSmem<R>::GWS;
-  const int side = blockIdx.z;  // 0: left volume / left guide, 1: right
+  // Dispatch order (blocks start in linear-index order): the tiles wholly inside the
+  // frame first, both sides, then the partial tiles of the last tile column and row.
+  // Warps of a partial tile that lie wholly outside the frame skip their work, so the
+  // last wave is made of cheap CTAs instead of full ones.
+  int tx, ty, side;  // side 0: left volume / left guide, 1: right
+  {
+    const int ntx = gridDim.x, nty = gridDim.y;
+    const int lin = blockIdx.x + ntx * (blockIdx.y + nty * blockIdx.z);
+    const int fx = a.W / kTX;                                // tile columns wholly inside
+    const int fy = min(nty, max(0, a.H / kTY - a.ty0));      // tile rows wholly inside
+    const int nfull = fx * fy, npart = ntx * nty - nfull;
+    if (lin < 2 * nfull) {
+      side = lin / nfull;
+      const int t = lin - side * nfull;
+      tx = t % fx;
+      ty = t / fx;
+    } else {
+      const int l2 = lin - 2 * nfull;
+      side = l2 / npart;
+      int t = l2 - side * npart;
+      const int ncol = fx < ntx ? fy : 0;  // the last column's tiles within the full rows
+      if (t < ncol) {
+        tx = fx;
+        ty = t;
+      } else {
+        t -= ncol;
+        tx = t % ntx;
+        ty = fy + t / ntx;
+      }
+    }
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int x0 = blockIdx.x * kTX, y0 = (a.ty0 + blockIdx.y) * kTY;
+  const int x0 = tx * kTX, y0 = (a.ty0 + ty) * kTY;
   const int wx = (warp % kNWX) * kPX, wy = (warp / kNWX) * kPY;
   const int sx = x0 + wx, sy = y0 + wy;
 
@@ -824,7 +854,8 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
 
   // ---- weights w'(p,q) = def_self(q) · ω_d(q-p) · ω_r(|i(q) - i(p)|), Eq.(6)-(8),
   //      their sum, and the window's column sums (EDGE denominators) ----
-  if (lane < kPX * kPY) {
+  const bool live = sx < a.W && sy < a.H;  // warp-uniform: the sub-tile has a pixel in the frame
+  if (live && lane < kPX * kPY) {
     const int py = lane / kPX, px = lane % kPX;
     // pixels outside the frame read the margin (kGuideUndef): their outputs are discarded
     float* wsm = sm.w[warp];
@@ -909,6 +940,7 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
       // the instruction cache (measured: MB2014 aggregation 14.3 -> 13.0 ms)
       __syncthreads();
     }
+    if (!live) continue;  // (still meets the per-d-block barriers)
     const int cls = cw_classify<R>(a, side, sx, sy, b, lane, sm.cwb[warp][b & 1]);
     __syncwarp();
     if (b + 1 <= b_hi) {
