@@ -357,6 +357,9 @@ def run_ours(args, cfg, rank, world, local_rank):
             "peak_source": f"148 SM x 128 FP32 lanes x 2 x {peak_src} (nominal); "
                            "FFMA2 microbenchmark 66.9 TFLOP/s (DESIGN.md §6)",
             "frac_of_ffma2_ceiling": round(achieved / FFMA2_CEILING_TFLOPS, 4),
+            "l1_bound": ("volume path: 0.69 L1 data-pipe wavefronts per FFMA2 (ncu per-instruction "
+                         "counts) cap k_agg at 72 % of FP32 peak before latency / prologue / tail "
+                         "losses (profiles/r02_agg_lsu_budget.txt, DESIGN.md §9b)") if args.path == "volume" else None,
             "useful_work": "numerator FMAs of Eq.(6): 2 sides x W*H*D*(2rho+1)^2 per launch",
             "denominator_forms": {k: round(v / max(1, sum(tiles.values())), 4) for k, v in tiles.items()}}
     base = None
