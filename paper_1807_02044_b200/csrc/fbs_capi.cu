@@ -32,10 +32,12 @@
 // with cudaErrorInvalidValue at launch.
 #ifdef FBS_EXP_ONLY_R4
 #define FBS_VOL_RADII(M) M(4)
+#define FBS_SD_RADII(M) M(4)
 #define FBS_WS_RADII(M) M(4)
 #define FBS_SYNC_RADII(M)
 #else
 #define FBS_VOL_RADII(M) M(0) M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8) M(9) M(10)
+#define FBS_SD_RADII(M) M(1) M(2) M(3) M(4) M(5)
 #define FBS_WS_RADII(M) M(0) M(1) M(2) M(3) M(4)
 #define FBS_SYNC_RADII(M) M(5) M(6)
 #endif
@@ -465,6 +467,13 @@ static fbs_ctx* create_volume(fbs_ctx* h) {
                        cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(vol::AggSmem<RR>));
   FBS_VOL_RADII(FBS_SMEM_ATTR)
 #undef FBS_SMEM_ATTR
+#define FBS_SMEM_ATTR_SD(RR)                                                                                  \
+  cudaFuncSetAttribute(vol::k_aggsd<RR, kVolEmpty, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                       sizeof(vol::AggSdSmem<RR>));                                                           \
+  cudaFuncSetAttribute(vol::k_aggsd<RR, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,            \
+                       sizeof(vol::AggSdSmem<RR>));
+  FBS_SD_RADII(FBS_SMEM_ATTR_SD)
+#undef FBS_SMEM_ATTR_SD
   cudaFuncSetAttribute(vol::k_cost, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)vol::cost_smem_bytes(4096 / kDB));
   if (cuda_check(cudaGetLastError(), "fbs_create smem attributes") != FBS_OK) {
@@ -602,7 +611,21 @@ static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0,
   {
     const dim3 grid((W + vol::kTX - 1) / vol::kTX, ty1 - ty0, 2);
     cudaError_t e = cudaErrorInvalidValue;
-    switch (R) {
+    // D <= 16 (Tsukuba-shaped): k_aggsd, 8-lane groups of 16 disparities, no padding;
+    // the disparity-range split and the sparse search range keep k_agg's KEYS / RANGED
+    const bool use_sd = vol::aggsd_ok(R, h->D) && !kq && !ranges;
+    if (use_sd) switch (R) {
+#define FBS_CASE_SD(RR)                                                                                       \
+  case RR:                                                                                                    \
+    e = aggR_exp ? launch_pdl(vol::k_aggsd<RR, false, true>, grid, dim3(vol::sd::kThreads),                   \
+                              sizeof(vol::AggSdSmem<RR>), s, a)                                               \
+                 : launch_pdl(vol::k_aggsd<RR, kVolEmpty, false>, grid, dim3(vol::sd::kThreads),              \
+                              sizeof(vol::AggSdSmem<RR>), s, a);                                              \
+    break;
+      FBS_SD_RADII(FBS_CASE_SD)
+#undef FBS_CASE_SD
+    }
+    else switch (R) {
 #define FBS_CASE(RR)                                                                                          \
   case RR:                                                                                                    \
     e = aggR_exp ? launch_pdl(vol::k_agg<RR, false, true>, grid, dim3(vol::AggGeom<RR>::THREADS),             \

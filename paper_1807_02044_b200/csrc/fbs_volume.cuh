@@ -1122,5 +1122,7 @@ __global__ void k_select_wta(const float* __restrict__ agg, int W, int H, int D,
   disp[p] = best > kSent ? d_min + bi : -1;
 }
 
+#include "fbs_aggsd.cuh"  // k_aggsd: D <= 16
+
 }  // namespace vol
 }  // namespace fbs
