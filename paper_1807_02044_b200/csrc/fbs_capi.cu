@@ -474,8 +474,10 @@ static fbs_ctx* create_volume(fbs_ctx* h) {
                        sizeof(vol::AggSdSmem<RR>));
   FBS_SD_RADII(FBS_SMEM_ATTR_SD)
 #undef FBS_SMEM_ATTR_SD
-  cudaFuncSetAttribute(vol::k_cost, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(vol::k_cost<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)vol::cost_smem_bytes(4096 / kDB));
+  cudaFuncSetAttribute(vol::k_cost<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)vol::cost_smem_bytes(1, 4));
   if (cuda_check(cudaGetLastError(), "fbs_create smem attributes") != FBS_OK) {
     free_all(h);
     delete h;
@@ -573,8 +575,13 @@ static int run_volume(fbs_ctx* h, const uint8_t* L, const uint8_t* Rimg, int r0,
     ca.L = L; ca.Rimg = Rimg; ca.volL = h->volL; ca.volR = h->volR;
     ca.bitsL = h->vbitsL; ca.bitsR = h->vbitsR; ca.Wb = h->vWb;
     ca.gpadL = h->gpadL; ca.gpadR = h->gpadR; ca.Wg = h->vWg;
-    const dim3 grd((W + vol::kCX - 1) / vol::kCX, c1 - c0, 2);
-    vol::k_cost<<<grd, 256, vol::cost_smem_bytes(h->nblk), s>>>(ca);
+    if (vol::cost_runs4(h->D)) {  // D <= 16: no padding slots computed
+      const int cx = vol::kCX * 4;
+      vol::k_cost<4><<<dim3((W + cx - 1) / cx, c1 - c0, 2), 256, vol::cost_smem_bytes(h->nblk, 4), s>>>(ca);
+    } else {
+      const dim3 grd((W + vol::kCX - 1) / vol::kCX, c1 - c0, 2);
+      vol::k_cost<1><<<grd, 256, vol::cost_smem_bytes(h->nblk), s>>>(ca);
+    }
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_check(e, "k_cost launch");  // nothing downstream runs on stale volumes
     h->launches += 1;

@@ -107,8 +107,13 @@ struct CostStage {
 // side 0: left volume c(x, x-d); side 1: right volume c(x'+d, x').  The same
 // function of the same operands (N · (r_self · r_other), a commutative product),
 // so right(u-d,v,d) == left(u,v,d) bit-exactly.
-template <int SIDE>
+// NRUN: runs of 8 pixels per warp.  NRUN = 1: a lane per disparity pair of a 64-slot
+// block (32 pairs); NRUN = 4 (D <= 16): 8 lanes per run (8 pairs = 16 disparities), four
+// runs per warp and a 4x wider CTA, so no lane computes padding slots (they keep the
+// undefined value the volumes were filled with at create).
+template <int SIDE, int NRUN>
 __device__ __forceinline__ void cost_side(const CostArgs& a, unsigned char* smraw) {
+  constexpr int kCX = vol::kCX * NRUN;  // pixels per CTA
   const int y = a.r0 + blockIdx.y;
   const int x0 = blockIdx.x * kCX;
   const int dspan = a.nblk * kDB;
@@ -169,10 +174,12 @@ __device__ __forceinline__ void cost_side(const CostArgs& a, unsigned char* smra
   // 3. values: warp <-> 8 consecutive pixels, lane <-> disparity pair.  The 3x3 dot
   // product is the sum of three column dots (one DP4A each); along the 8 pixels a
   // column dot is shared by three blocks, so 10 DP4A give 8 dot products.
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane32 = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int LPR = 32 / NRUN;         // lanes per run
+  const int lane = lane32 % LPR;         // disparity pair within the run
   float* vol = SIDE == 0 ? a.volL : a.volR;
-  constexpr int PPW = kCX / 8;
-  const int xw = warp * PPW;
+  constexpr int PPW = vol::kCX / 8;      // pixels per run
+  const int xw = (warp * NRUN + lane32 / LPR) * PPW;
   const int npx = min(PPW, a.W - (x0 + xw));
   if (npx <= 0) return;
   float* vp = vol + vol_at(y + a.R - a.vbase, 0, x0 + xw + a.R, a.nblk, a.Wv) + 2 * lane;
@@ -231,9 +238,11 @@ __device__ __forceinline__ void cost_side(const CostArgs& a, unsigned char* smra
   }
 }
 
-__host__ __device__ constexpr size_t cost_smem_bytes(int nblk) {
-  return (size_t)(kCX + 2 + kCX + nblk * kDB + 1) * 12 + 8 + (size_t)(kCX + kCX + nblk * kDB - 1) * 8;
+__host__ __device__ constexpr size_t cost_smem_bytes(int nblk, int nrun = 1) {
+  return (size_t)(kCX * nrun + 2 + kCX * nrun + nblk * kDB + 1) * 12 + 8 +
+         (size_t)(kCX * nrun + kCX * nrun + nblk * kDB - 1) * 8;
 }
+constexpr bool cost_runs4(int D) { return D <= 16; }  // k_cost<4>: 8 lanes x 2 disparities per run
 
 // grid: (ceil(W/kCX), r1-r0, 2 sides); block 256 = 8 warps; warp <-> pixel, lane <-> d pair.
 // k_cost is issue-bound (~75 % issue active, the rest barrier / load stalls): a
@@ -242,11 +251,12 @@ __host__ __device__ constexpr size_t cost_smem_bytes(int nblk) {
 #ifndef FBS_KCOST_MINB
 #define FBS_KCOST_MINB 5
 #endif
+template <int NRUN>
 __global__ void __launch_bounds__(256, FBS_KCOST_MINB) k_cost(CostArgs a) {
   extern __shared__ __align__(16) unsigned char csm[];
   pdl_trigger();  // k_agg may be scheduled now; it waits for our results in pdl_wait()
-  if (blockIdx.z == 0) cost_side<0>(a, csm);
-  else cost_side<1>(a, csm);
+  if (blockIdx.z == 0) cost_side<0, NRUN>(a, csm);
+  else cost_side<1, NRUN>(a, csm);
 }
 
 // fill a buffer with a float value (volume margins = kUndef)
