@@ -186,10 +186,11 @@ def test_select_stage_matches_oracle_on_same_volumes(fbs, oracle_lib):
 
 
 @pytest.mark.parametrize("path", PATHS)
-def test_row_bands_bit_identical(fbs, path):
+@pytest.mark.parametrize("cname", ["teddy", "tsukuba"])  # tsukuba: D <= 16 kernels (k_aggsd, k_cost<4>)
+def test_row_bands_bit_identical(fbs, path, cname):
     """fbs_compute_rows over any band split stitches to fbs_compute exactly
     (the per-output arithmetic does not depend on the band origin)."""
-    cfg = synth.CONFIGS["teddy"]
+    cfg = synth.CONFIGS[cname]
     L, R = synth.frame(cfg, 0)
     m = fbs.FBS(cfg.W, cfg.H, cfg.d_min, cfg.d_max, cfg.radius, cfg.gamma_d, cfg.gamma_r, path=path)
     Ld, Rd = to_dev(L), to_dev(R)
