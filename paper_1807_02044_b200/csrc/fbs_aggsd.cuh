@@ -213,14 +213,17 @@ __global__ void __launch_bounds__(sd::kThreads, 3) k_aggsd(const AggArgs a) {
         gv[t] = dy < K1 ? gq[dy * GWS + dx] : 0.f;
       }
 #pragma unroll
-      for (int t = 0; t < NB; ++t) {
+      for (int t = 0; t < NB; ++t) {  // adjacent taps of a row in pairs (k_agg's tap_pair)
         const int dy = dy0 + t / K1, dx = t % K1;
-        if (dy < K1) {
-          const float dd = __fsub_rn(gv[t], gp);
-          float w;
-          asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(w) : "f"(__fmaf_rn(__fmul_rn(dd, dd), a.nkr, a.cd[dy * K1 + dx])));
-          col[dx] = __fadd_rn(col[dx], w);
-          wp[(dy * K1 + dx) * 16] = w;
+        if (dy >= K1 || (dx & 1)) continue;
+        if (dx + 1 < K1) {
+          float w0, w1;
+          tap_pair(gv[t], gv[t + 1], gp, a.nkr, a.cd[dy * K1 + dx], a.cd[dy * K1 + dx + 1], w0, w1, col[dx],
+                   col[dx + 1]);
+          wp[(dy * K1 + dx) * 16] = w0;
+          wp[(dy * K1 + dx + 1) * 16] = w1;
+        } else {
+          wp[(dy * K1 + dx) * 16] = tap_one(gv[t], gp, a.nkr, a.cd[dy * K1 + dx], col[dx]);
         }
       }
     }

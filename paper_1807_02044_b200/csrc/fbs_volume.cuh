@@ -608,6 +608,37 @@ __device__ __forceinline__ float rcp_nr(float x) {
   return __fmul_rn(r, __fmaf_rn(-x, r, 2.0f));
 }
 
+// Weights w' = 2^(cd + nkr Δ²) (Eq.(7)(8); Δ² exact, one MUFU.EX2 per tap) of the two
+// adjacent taps (dy, dx), (dy, dx+1) of a prologue row, their arithmetic as f32x2 (the
+// same per-element roundings as the scalar form, half the issue slots), and the taps'
+// column sums advanced as one pair.
+__device__ __forceinline__ void tap_pair(float g0, float g1, float gp, float nkr, float cd0, float cd1,
+                                         float& w0, float& w1, float& col0, float& col1) {
+  unsigned long long G, P, D2, NK, CD, C, CL, WP;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(G) : "f"(g0), "f"(g1));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(P) : "f"(-gp));
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(D2) : "l"(G), "l"(P));
+  asm("mul.rn.f32x2 %0, %0, %0;" : "+l"(D2));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(NK) : "f"(nkr));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(CD) : "f"(cd0), "f"(cd1));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(C) : "l"(D2), "l"(NK), "l"(CD));
+  float c0, c1;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(c0), "=f"(c1) : "l"(C));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(w0) : "f"(c0));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(w1) : "f"(c1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(CL) : "f"(col0), "f"(col1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(WP) : "f"(w0), "f"(w1));
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(CL) : "l"(WP));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(col0), "=f"(col1) : "l"(CL));
+}
+__device__ __forceinline__ float tap_one(float g, float gp, float nkr, float cd, float& col) {
+  const float dd = __fsub_rn(g, gp);
+  float w;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(w) : "f"(__fmaf_rn(__fmul_rn(dd, dd), nkr, cd)));
+  col = __fadd_rn(col, w);
+  return w;
+}
+
 // Order-preserving map float -> u32 (larger float <=> larger key).
 __device__ __forceinline__ unsigned fkey(float v) {
   const unsigned b = __float_as_uint(v);
@@ -890,16 +921,20 @@ __global__ void __launch_bounds__(AggGeom<R>::THREADS, AggGeom<R>::MINB) k_agg(c
         const int dy = dy0 + t / K1, dx = t % K1;
         gv[t] = dy < K1 ? gq[dy * GWS + dx] : 0.f;
       }
+      // ω_d ω_r = 2^(cd(dx,dy) + nkr Δ²), adjacent taps of a row in pairs
 #pragma unroll
       for (int t = 0; t < NB; ++t) {
         const int dy = dy0 + t / K1, dx = t % K1;
-        if (dy < K1) {
-          // ω_d ω_r = 2^(cd(dx,dy) + nkr Δ²): Δ² exact, one MUFU.EX2 per tap
-          const float dd = __fsub_rn(gv[t], gp);
-          float w;
-          asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(w) : "f"(__fmaf_rn(__fmul_rn(dd, dd), a.nkr, a.cd[dy * K1 + dx])));
-          col[dx] = __fadd_rn(col[dx], w);
-          wsm[((py * K1 + dy) * K1 + dx) * kPX + px] = w;
+        if (dy >= K1 || (dx & 1)) continue;
+        float* wr = wsm + ((py * K1 + dy) * K1 + dx) * kPX + px;
+        if (dx + 1 < K1) {
+          float w0, w1;
+          tap_pair(gv[t], gv[t + 1], gp, a.nkr, a.cd[dy * K1 + dx], a.cd[dy * K1 + dx + 1], w0, w1, col[dx],
+                   col[dx + 1]);
+          wr[0] = w0;
+          wr[kPX] = w1;
+        } else {
+          wr[0] = tap_one(gv[t], gp, a.nkr, a.cd[dy * K1 + dx], col[dx]);
         }
       }
     }
