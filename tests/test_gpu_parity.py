@@ -150,6 +150,38 @@ def test_all_radii(fbs, oracle_lib, rho, path):
         assert np.array_equal(al.view(np.uint32), cl.view(np.uint32))
 
 
+SMALL_D = [(r, dmax) for r in range(1, 6) for dmax in (15, 8)]
+
+
+@pytest.mark.parametrize("rho,d_max", SMALL_D, ids=[f"{r}-D{d + 1}" for r, d in SMALL_D])
+def test_small_d_radii(fbs, oracle_lib, rho, d_max):
+    """D <= 16 runs k_aggsd + k_cost<4> (volume path): element-wise aggregated volumes,
+    maps and subpixel against the oracle at every radius they serve, D = 16 and a
+    ragged D = 9 (padding inside the 16-disparity group)."""
+    W, H, d_min = 70, 36, 0
+    L, R = make_pair("layered", W, H, d_min, d_max, 60 + rho + d_max)
+    ref = oracle_lib.fbs(L, R, d_min, d_max, rho, 4.0, 30.0)
+    m = fbs.FBS(W, H, d_min, d_max, rho, 4.0, 30.0)
+    Ld, Rd = to_dev(L), to_dev(R)
+    vols, emaps = m.volumes(Ld, Rd, maps=True)
+    cl, cr, al, ar = (v.cpu().numpy() for v in vols)
+    parity.check_volume(cl, ref.cost_l, 1e-6, "cost_l")
+    parity.check_volume(cr, ref.cost_r, 1e-6, "cost_r")
+    floor = parity.agg_abs_floor(rho)
+    e_al = parity.check_volume(al, ref.agg_l, floor, "agg_l")
+    e_ar = parity.check_volume(ar, ref.agg_r, floor, "agg_r")
+    out, dl, dr = (t.cpu().numpy() for t in m.maps(Ld, Rd))
+    for a_, b_ in zip((out, dl, dr), (t.cpu().numpy() for t in emaps)):  # production == exporting kernel
+        assert np.array_equal(a_.view(np.uint32), b_.view(np.uint32))
+    rep = parity.MapReport()
+    D = d_max - d_min + 1
+    parity.check_int_map(dl, ref.disp_l, lambda i, d: ref.agg_l.reshape(-1, D)[i, d - d_min], "d_L", rep)
+    parity.check_int_map(dr, ref.disp_r, lambda i, d: ref.agg_r.reshape(-1, D)[i, d - d_min], "d_R", rep)
+    parity.check_final(out, ref.disp, dl, ref.disp_l, dr, ref.disp_r, ref.sub_den, W, rep)
+    log_errors(f"small-d-{rho}-D{D}/volume", agg_l=e_al, agg_r=e_ar, subpix=rep.max_subpix_err,
+               near_ties=rep.near_ties, pixels=W * H)
+
+
 @pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("s", [0, 7, 15])
 def test_known_shift_exact(fbs, s, path):
